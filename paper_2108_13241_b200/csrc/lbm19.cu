@@ -1,0 +1,1244 @@
+// liblbm19 -- B200-native D3Q19 fused pull stream + BGK collide (sm_100a).
+//
+// Drop-in replacement for the reference's compiled step operator
+// (pkg/src/sparselbm/kernel.py:56-141) and the Simulation plumbing around it;
+// the C-ABI is declared in include/lbm19.h.  Kernels:
+//
+//   k_flags        node descriptors -> packed u32 flag word per slot (mask,
+//                  type, orientation, bc index); layouts.py:173-188 on device
+//   k_tile_keep / k_tile_compact
+//                  sparse tile index: kept-tile flags, exclusive scan (CUB),
+//                  compacted (tx,ty,tz) list and the 27-entry neighbour table
+//                  (layouts.py:263-269, 389-401 generalised)
+//   k_init         float64 equilibrium, cast to the storage type (kernel.py:190-237)
+//   k_step_dense   ONE fused pass per step: pull gather with link-wise bounce-back,
+//                  Zou-He closures, moments, BGK, node-local store (kernel.py:72-141)
+//   k_step_tile    the same over the compacted tile list + nbr27
+//   k_macro / k_mass / k_nonfinite / k_get_pdf / k_set_pdf   readbacks
+//
+// Storage (HBM): two buffers, each (19, plane_stride) in the storage type.
+//   dense: slot(x,y,z) = ((z+1)*ny + y)*nxp + x, nxp = nx rounded up to 32,
+//          one ghost plane below and above (z-slab halos / periodic wrap);
+//   tile:  slot = rank*TN + ((lz*ey + ly)*ex + lx), each (tile, direction)
+//          block contiguous (8^3 fp32 -> 2 KB).
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "d3q19.cuh"
+#include "lbm19.h"
+
+using namespace lbm;
+
+// ------------------------------------------------------------ error plumbing
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      if (e_ == cudaErrorMemoryAllocation) {                                          \
+        cudaGetLastError();                                                           \
+        return fail(LBM_ENOMEM, "%s: %s", #call, cudaGetErrorString(e_));             \
+      }                                                                               \
+      return fail(LBM_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                          \
+    }                                                                                 \
+  } while (0)
+
+#define CKL() CK(cudaGetLastError())
+
+// ------------------------------------------------------------- device params
+struct Geo {
+  int nx, ny, nz, nxp;     // extents; nxp = padded row pitch (dense)
+  long long plane;         // ny * nxp (dense)
+  long long ps;            // elements between direction planes
+  int px, py, pzw;         // periodic x, y; wrap z inside this handle
+  int tiled;               // tile layout?
+  int ex, ey, ez, lex, ley, lez;  // tile edges and their log2
+  int gx, gy, gz;          // tile grid
+  int tn;                  // nodes per tile
+};
+
+struct SlotMap {
+  const int* rank;  // tile rank grid (gz, gy, gx), -1 = not allocated (tile layouts)
+  __device__ __forceinline__ long long slot(const Geo& g, int x, int y, int z) const {
+    if (!g.tiled) return ((long long)(z + 1) * g.ny + y) * g.nxp + x;
+    const int tx = x >> g.lex, ty = y >> g.ley, tz = z >> g.lez;
+    const int r = rank[((long long)tz * g.gy + ty) * g.gx + tx];
+    if (r < 0) return -1;
+    const int l = (((z & (g.ez - 1)) << g.ley) + (y & (g.ey - 1))) << g.lex | (x & (g.ex - 1));
+    return (long long)r * g.tn + l;
+  }
+  // flag-array index of a slot (dense flags carry no ghost planes)
+  __device__ __forceinline__ long long flag_index(const Geo& g, long long s) const {
+    return g.tiled ? s : s - g.plane;
+  }
+};
+
+// --------------------------------------------------------------- geometry
+__device__ __forceinline__ uint32_t type_at(const uint8_t* __restrict__ type,
+                                            const uint8_t* __restrict__ glo,
+                                            const uint8_t* __restrict__ ghi, const Geo& g, int x,
+                                            int y, int z) {
+  // returns 0 (SOLID / absent) outside the domain on non-periodic axes
+  if (x < 0 || x >= g.nx) {
+    if (!g.px) return SOLID;
+    x = x < 0 ? x + g.nx : x - g.nx;
+  }
+  if (y < 0 || y >= g.ny) {
+    if (!g.py) return SOLID;
+    y = y < 0 ? y + g.ny : y - g.ny;
+  }
+  if (z < 0) return glo ? glo[(long long)y * g.nx + x] : SOLID;
+  if (z >= g.nz) return ghi ? ghi[(long long)y * g.nx + x] : SOLID;
+  return type[((long long)z * g.ny + y) * g.nx + x];
+}
+
+__device__ __forceinline__ uint32_t node_flag(const uint8_t* __restrict__ type,
+                                              const uint8_t* __restrict__ orient,
+                                              const int* __restrict__ bcidx,
+                                              const uint8_t* __restrict__ glo,
+                                              const uint8_t* __restrict__ ghi, const Geo& g,
+                                              int x, int y, int z, int nb, int* err) {
+  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const uint32_t t = type[n];
+  const uint32_t o = orient[n];
+  const int b = bcidx[n];
+  if (t > PRESSURE_BC || o > O_BOTTOM) atomicOr(err, 1);
+  if ((t == VELOCITY_BC || t == PRESSURE_BC) && (b < 0 || b >= nb || o == O_NONE)) atomicOr(err, 2);
+  uint32_t m = 0;
+  if (t != SOLID) {
+#pragma unroll
+    for (int j = 1; j < Q; ++j)
+      if (type_at(type, glo, ghi, g, x + cx(j), y + cy(j), z + cz(j)) != SOLID) m |= 1u << (j - 1);
+  }
+  return make_flag(m, t, o, b < 0 ? 0u : (uint32_t)b);
+}
+
+// dense: one thread per (padded) flag entry
+__global__ void k_flags_dense(uint32_t* __restrict__ flags, const uint8_t* __restrict__ type,
+                              const uint8_t* __restrict__ orient, const int* __restrict__ bcidx,
+                              const uint8_t* __restrict__ glo, const uint8_t* __restrict__ ghi,
+                              Geo g, int nb, int* err, unsigned long long* nonsolid) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nxp) return;
+  uint32_t w = 0;
+  if (x < g.nx) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
+  flags[((long long)z * g.ny + y) * g.nxp + x] = w;
+  const unsigned c = __popc(__ballot_sync(0xffffffffu, flag_type(w) != SOLID));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
+}
+
+// tiles: one warp per tile of the full tile grid -> keep flag
+__global__ void k_tile_keep(int* __restrict__ keep, const uint8_t* __restrict__ type, Geo g,
+                            int keep_all, long long ntiles) {
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  int any = 0;
+  if (keep_all) {
+    any = 1;
+  } else {
+    const int tx = (int)(t % g.gx), ty = (int)((t / g.gx) % g.gy), tz = (int)(t / ((long long)g.gx * g.gy));
+    for (int l = lane; l < g.tn && !any; l += 32) {
+      const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
+      const int x = tx * g.ex + lx, y = ty * g.ey + ly, z = tz * g.ez + lz;
+      if (x < g.nx && y < g.ny && z < g.nz && type[((long long)z * g.ny + y) * g.nx + x] != SOLID) any = 1;
+    }
+    any = __any_sync(0xffffffffu, any);
+  }
+  if (lane == 0) keep[t] = any;
+}
+
+__global__ void k_tile_compact(int* __restrict__ rank, const int* __restrict__ keep,
+                               const int* __restrict__ scan, int* __restrict__ tiles, Geo g,
+                               long long ntiles) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  if (keep[t]) {
+    const int r = scan[t];
+    rank[t] = r;
+    tiles[3LL * r + 0] = (int)(t % g.gx);
+    tiles[3LL * r + 1] = (int)((t / g.gx) % g.gy);
+    tiles[3LL * r + 2] = (int)(t / ((long long)g.gx * g.gy));
+  } else {
+    rank[t] = -1;
+  }
+}
+
+__global__ void k_tile_nbr(int* __restrict__ nbr, const int* __restrict__ tiles,
+                           const int* __restrict__ rank, Geo g, long long T) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= T * 27) return;
+  const long long t = k / 27;
+  const int c = (int)(k % 27);
+  const int dx = c % 3 - 1, dy = (c / 3) % 3 - 1, dz = c / 9 - 1;
+  int qx = tiles[3 * t] + dx, qy = tiles[3 * t + 1] + dy, qz = tiles[3 * t + 2] + dz;
+  int v = -1;
+  bool ok = true;
+  if (qx < 0 || qx >= g.gx) { if (g.px) qx = (qx + g.gx) % g.gx; else ok = false; }
+  if (qy < 0 || qy >= g.gy) { if (g.py) qy = (qy + g.gy) % g.gy; else ok = false; }
+  if (qz < 0 || qz >= g.gz) { if (g.pzw) qz = (qz + g.gz) % g.gz; else ok = false; }
+  if (ok) v = rank[((long long)qz * g.gy + qy) * g.gx + qx];
+  nbr[k] = v;
+}
+
+// tiles: one thread per slot of the kept tiles
+__global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict__ tiles,
+                             const uint8_t* __restrict__ type, const uint8_t* __restrict__ orient,
+                             const int* __restrict__ bcidx, const uint8_t* __restrict__ glo,
+                             const uint8_t* __restrict__ ghi, Geo g, long long nslots, int nb,
+                             int* err, unsigned long long* nonsolid) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t w = 0;
+  if (s < nslots) {
+    const long long t = s / g.tn;
+    const int l = (int)(s - t * g.tn);
+    const int x = tiles[3 * t] * g.ex + (l & (g.ex - 1));
+    const int y = tiles[3 * t + 1] * g.ey + ((l >> g.lex) & (g.ey - 1));
+    const int z = tiles[3 * t + 2] * g.ez + (l >> (g.lex + g.ley));
+    if (x < g.nx && y < g.ny && z < g.nz) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
+    flags[s] = w;
+  }
+  const unsigned c = __popc(__ballot_sync(0xffffffffu, s < nslots && flag_type(w) != SOLID));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
+}
+
+// ------------------------------------------------------------ init / readback
+template <typename T>
+__global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
+                       const double* __restrict__ rho, const double* __restrict__ ux,
+                       const double* __restrict__ uy, const double* __restrict__ uz, double rho0,
+                       double ux0, double uy0, double uz0, const uint8_t* __restrict__ bckind,
+                       const double* __restrict__ bcv, const double* __restrict__ bcr, int nb) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long s = sm.slot(g, x, y, z);
+  if (s < 0) return;
+  const uint32_t w = flags[sm.flag_index(g, s)];
+  const uint32_t t = flag_type(w);
+  if (t == SOLID) return;
+  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  double r = rho ? rho[n] : rho0, vx = ux ? ux[n] : ux0, vy = uy ? uy[n] : uy0, vz = uz ? uz[n] : uz0;
+  const int b = (int)flag_bc(w);
+  if (t == VELOCITY_BC && b < nb && bckind[b] == 0) {
+    vx = bcv[3 * b];
+    vy = bcv[3 * b + 1];
+    vz = bcv[3 * b + 2];
+  } else if (t == PRESSURE_BC && b < nb && bckind[b] == 1) {
+    r = bcr[b];
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) pre[(long long)i * g.ps + s] = (T)init_eq(i, r, vx, vy, vz);
+}
+
+template <typename T>
+__global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
+                        Geo g, double* __restrict__ rho, double* __restrict__ ux,
+                        double* __restrict__ uy, double* __restrict__ uz) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const long long s = sm.slot(g, x, y, z);
+  double r = 0, vx = 0, vy = 0, vz = 0;
+  if (s >= 0 && flag_type(flags[sm.flag_index(g, s)]) != SOLID) {
+    double f[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = (double)pre[(long long)i * g.ps + s];
+    using A = ar<double>;
+    r = density19(f);
+    if (r != 0.0) {
+      double mx, my, mz;
+      momentum19(f, mx, my, mz);
+      vx = A::div(mx, r);
+      vy = A::div(my, r);
+      vz = A::div(mz, r);
+    }
+  }
+  if (rho) rho[n] = r;
+  if (ux) ux[n] = vx;
+  if (uy) uy[n] = vy;
+  if (uz) uz[n] = vz;
+}
+
+template <typename T>
+__global__ void k_get_pdf(const T* __restrict__ buf, SlotMap sm, Geo g, T* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const long long s = sm.slot(g, x, y, z);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) out[i * N + n] = s >= 0 ? buf[(long long)i * g.ps + s] : (T)0;
+}
+
+template <typename T>
+__global__ void k_set_pdf(T* __restrict__ buf, SlotMap sm, Geo g, const T* __restrict__ in) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const long long s = sm.slot(g, x, y, z);
+  if (s < 0) return;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) buf[(long long)i * g.ps + s] = in[i * N + n];
+}
+
+__global__ void k_slot_of(SlotMap sm, Geo g, int* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  out[((long long)z * g.ny + y) * g.nx + x] = (int)sm.slot(g, x, y, z);
+}
+
+__global__ void k_get_flags(const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
+                            uint32_t* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long s = sm.slot(g, x, y, z);
+  out[((long long)z * g.ny + y) * g.nx + x] = s >= 0 ? flags[sm.flag_index(g, s)] : 0u;
+}
+
+// first non-finite value of `pre` in (direction, visit order); visit order is
+// canonical for dense layouts and tile-major for tile layouts
+template <typename T>
+__global__ void k_nonfinite(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
+                            Geo g, long long V, unsigned long long* best) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nx) return;
+  const long long s = sm.slot(g, x, y, z);
+  if (s < 0 || flag_type(flags[sm.flag_index(g, s)]) == SOLID) return;
+  const long long v = g.tiled ? s : ((long long)z * g.ny + y) * g.nx + x;
+  for (int i = 0; i < Q; ++i) {
+    const T val = pre[(long long)i * g.ps + s];
+    if (!isfinite((double)val)) {
+      atomicMin(best, (unsigned long long)(i * V + v));
+      return;
+    }
+  }
+}
+
+// deterministic two-pass mass reduction: per-block partial sums, then one block
+template <typename T>
+__global__ void k_mass_partial(const T* __restrict__ pre, const uint32_t* __restrict__ flags, Geo g,
+                               long long nflags, double* __restrict__ partial) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nflags;
+       k += (long long)gridDim.x * blockDim.x) {
+    if (flag_type(flags[k]) == SOLID) continue;
+    const long long s = g.tiled ? k : k + g.plane;
+    double a = 0.0;
+    for (int i = 0; i < Q; ++i) a += (double)pre[(long long)i * g.ps + s];
+    acc += a;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_mass_final(const double* __restrict__ partial, int n, double* out) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += partial[k];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+// ------------------------------------------------------------------ steps
+// Solid lanes complete the 32-B sectors of their non-solid neighbours with
+// zeros (the values they already hold), so every store is a full sector.
+template <typename T>
+__device__ __forceinline__ bool sector_needs_zero(bool nonsolid) {
+  constexpr int SEC = 32 / (int)sizeof(T);
+  const unsigned act = __ballot_sync(0xffffffffu, nonsolid);
+  const int lane = threadIdx.x & 31;
+  const unsigned grp = ((1u << SEC) - 1u) << (lane & ~(SEC - 1));
+  return (act & grp) != 0u;
+}
+
+template <typename T>
+__device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
+                                                 const T* __restrict__ bcr, T om,
+                                                 T* __restrict__ post, long long ps, long long s) {
+  const uint32_t t = flag_type(w);
+  if (t == VELOCITY_BC) {
+    const uint32_t b = flag_bc(w);
+    zou_he_velocity19<T>(f, flag_orient(w), bcv[3 * b], bcv[3 * b + 1], bcv[3 * b + 2]);
+  } else if (t == PRESSURE_BC) {
+    zou_he_pressure19<T>(f, flag_orient(w), bcr[flag_bc(w)]);
+  }
+  T rho, vx, vy, vz;
+  moments19(f, rho, vx, vy, vz);
+  collide19(f, rho, vx, vy, vz, om);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) post[(long long)i * ps + s] = f[i];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_step_dense(const T* __restrict__ pre, T* __restrict__ post,
+                                                   const uint32_t* __restrict__ flags,
+                                                   const T* __restrict__ bcv,
+                                                   const T* __restrict__ bcr, Geo g, T om) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
+  const int fi = (z * g.ny + y) * g.nxp + x;
+  const int s = fi + (int)g.plane;
+  const uint32_t w = flags[fi];
+  const bool live = flag_type(w) != SOLID;
+  const bool zfill = sector_needs_zero<T>(live);
+  if (!live) {
+    if (zfill) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) post[(long long)i * g.ps + s] = (T)0;
+    }
+    return;
+  }
+  // offsets to the upstream node x - c_i along each axis (wrap on periodic axes)
+  const int xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
+  const int xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
+  const int ym = y == 0 ? (g.py ? (g.ny - 1) * g.nxp : 0) : -g.nxp;
+  const int yp = y == g.ny - 1 ? (g.py ? -(g.ny - 1) * g.nxp : 0) : g.nxp;
+  const int pl = (int)g.plane;
+  const int zm = (z == 0 && g.pzw) ? (g.nz - 1) * pl : -pl;
+  const int zp = (z == g.nz - 1 && g.pzw) ? -(g.nz - 1) * pl : pl;
+  T f[Q];
+  f[0] = __ldg(pre + s);
+#pragma unroll
+  for (int i = 1; i < Q; ++i) {
+    const int o = opp(i);
+    const int off = (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0)) +
+                    (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0)) +
+                    (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0));
+    const bool present = (w >> (o - 1)) & 1u;
+    const T* src = present ? pre + (long long)i * g.ps + (s + off) : pre + (long long)o * g.ps + s;
+    f[i] = __ldg(src);
+  }
+  bc_collide_store<T>(f, w, bcv, bcr, om, post, g.ps, s);
+}
+
+template <typename T>
+__global__ void k_step_tile(const T* __restrict__ pre, T* __restrict__ post,
+                            const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
+                            const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om) {
+  __shared__ int snbr[27];
+  const int t = blockIdx.x;
+  if (threadIdx.x < 27) snbr[threadIdx.x] = nbr27[27LL * t + threadIdx.x];
+  __syncthreads();
+  for (int l = threadIdx.x; l < g.tn; l += blockDim.x) {
+    const long long s = (long long)t * g.tn + l;
+    const uint32_t w = flags[s];
+    const bool live = flag_type(w) != SOLID;
+    const bool z0 = sector_needs_zero<T>(live);
+    if (!live) {
+      if (z0) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) post[(long long)i * g.ps + s] = (T)0;
+      }
+      continue;
+    }
+    const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
+    T f[Q];
+    f[0] = __ldg(pre + s);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      const int o = opp(i);
+      const bool present = (w >> (o - 1)) & 1u;
+      long long idx;
+      if (present) {
+        const int sx = lx - cx(i), sy = ly - cy(i), sz = lz - cz(i);
+        const int dx = sx < 0 ? -1 : (sx >= g.ex ? 1 : 0);
+        const int dy = sy < 0 ? -1 : (sy >= g.ey ? 1 : 0);
+        const int dz = sz < 0 ? -1 : (sz >= g.ez ? 1 : 0);
+        const int nt = snbr[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
+        const int sl = (((sz & (g.ez - 1)) << g.ley) + (sy & (g.ey - 1))) << g.lex | (sx & (g.ex - 1));
+        idx = (long long)i * g.ps + (long long)nt * g.tn + sl;
+      } else {
+        idx = (long long)o * g.ps + s;
+      }
+      f[i] = __ldg(pre + idx);
+    }
+    bc_collide_store<T>(f, w, bcv, bcr, om, post, g.ps, s);
+  }
+}
+
+// ----------------------------------------------------------------- handle
+struct lbm_handle {
+  lbm_desc d{};
+  int esize = 4;
+  Geo g{};
+  SlotMap sm{nullptr};
+  long long n_nodes = 0, n_slots = 0, nflags = 0;
+  long long n_tiles = 0, ntiles_grid = 0;
+  long long n_nonsolid = 0;
+  void* f[2] = {nullptr, nullptr};
+  uint32_t* flags = nullptr;
+  int* rank = nullptr;    // tile rank grid
+  int* tiles = nullptr;   // (T, 3)
+  int* nbr27 = nullptr;   // (T, 27)
+  void* bcv = nullptr;    // (nb, 3) storage type
+  void* bcr = nullptr;    // (nb) storage type
+  uint8_t* bckind64 = nullptr;
+  double* bcv64 = nullptr;
+  double* bcr64 = nullptr;
+  int nb = 0;
+  int parity = 0;
+  bool geometry = false, initialized = false;
+  long long step_count = 0, visited_total = 0, launches = 0;
+  long long device_bytes = 0;
+  double last_ms = 0.0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double* scratch = nullptr;   // reductions
+  unsigned long long* uscratch = nullptr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int ilog2(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+
+template <typename P>
+int dev_alloc(lbm_handle* h, P** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LBM_ENOMEM : LBM_ECUDA,
+                "cudaMalloc(%zu bytes): %s", bytes, cudaGetErrorString(e));
+  }
+  h->device_bytes += (long long)bytes;
+  *p = (P*)q;
+  return 0;
+}
+
+void dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+void free_geometry(lbm_handle* h) {
+  dev_free(h->f[0]);
+  dev_free(h->f[1]);
+  dev_free(h->flags);
+  dev_free(h->rank);
+  dev_free(h->tiles);
+  dev_free(h->nbr27);
+  dev_free(h->bcv);
+  dev_free(h->bcr);
+  dev_free(h->bckind64);
+  dev_free(h->bcv64);
+  dev_free(h->bcr64);
+  h->f[0] = h->f[1] = nullptr;
+  h->flags = nullptr;
+  h->rank = h->tiles = h->nbr27 = nullptr;
+  h->bcv = h->bcr = nullptr;
+  h->bckind64 = nullptr;
+  h->bcv64 = h->bcr64 = nullptr;
+  h->device_bytes = 0;
+  h->geometry = h->initialized = false;
+}
+
+bool is_tiled(int layout) { return layout == LBM_LAYOUT_TILE || layout == LBM_LAYOUT_POINTER_TILE; }
+
+dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g.nz); }
+
+template <typename T>
+int launch_step(lbm_handle* h, const void* pre, void* post) {
+  const Geo& g = h->g;
+  const T om = (T)h->d.omega;
+  if (!g.tiled) {
+    const int bx = 128;
+    dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
+    k_step_dense<T><<<grid, bx, 0, h->stream>>>((const T*)pre, (T*)post, h->flags,
+                                                 (const T*)h->bcv, (const T*)h->bcr, g, om);
+  } else {
+    if (h->n_tiles == 0) return 0;
+    const int bt = g.tn < 512 ? g.tn : 512;
+    k_step_tile<T><<<(unsigned)h->n_tiles, bt, 0, h->stream>>>(
+        (const T*)pre, (T*)post, h->flags, h->nbr27, (const T*)h->bcv, (const T*)h->bcr, g, om);
+  }
+  h->launches += 1;
+  return 0;
+}
+
+}  // namespace
+
+// ================================================================= C-ABI
+extern "C" {
+
+const char* lbm_last_error(void) { return g_err.c_str(); }
+int lbm_abi_version(void) { return LBM_ABI_VERSION; }
+
+int lbm_device_count(int* n) {
+  if (!n) return fail(LBM_EINVAL, "n is NULL");
+  CK(cudaGetDeviceCount(n));
+  return 0;
+}
+
+int lbm_create(const lbm_desc* desc, lbm_t** out) {
+  if (!desc || !out) return fail(LBM_EINVAL, "desc/out is NULL");
+  const lbm_desc& d = *desc;
+  if (d.nx <= 0 || d.ny <= 0 || d.nz <= 0)
+    return fail(LBM_EINVAL, "dims must be positive, got (%d, %d, %d)", d.nx, d.ny, d.nz);
+  if (d.dtype != LBM_F32 && d.dtype != LBM_F64) return fail(LBM_EINVAL, "dtype must be LBM_F32 or LBM_F64");
+  if (d.layout < 0 || d.layout > LBM_LAYOUT_POINTER_TILE) return fail(LBM_EINVAL, "unknown layout %d", d.layout);
+  if (!(d.omega > 0.0 && d.omega < 2.0)) return fail(LBM_EINVAL, "omega must lie in (0, 2), got %g", d.omega);
+  const int nzg = d.nz_global > 0 ? d.nz_global : d.nz;
+  if (d.z0 < 0 || d.z0 + d.nz > nzg) return fail(LBM_EINVAL, "slab [%d, %d) outside nz_global %d", d.z0, d.z0 + d.nz, nzg);
+  if (!is_tiled(d.layout) && (long long)(d.nz + 2) * d.ny * ((d.nx + 31) / 32 * 32) >= (1LL << 31))
+    return fail(LBM_EINVAL, "dense slab of %d x %d x %d nodes exceeds 2^31 slots; split it into z-slabs", d.nx, d.ny, d.nz);
+  if (is_tiled(d.layout)) {
+    for (int a = 0; a < 3; ++a) {
+      const int e = d.tile[a];
+      if (e < 1 || (e & (e - 1))) return fail(LBM_EINVAL, "tile edges must be powers of two, got %d", e);
+    }
+    if (d.tile[0] * d.tile[1] * d.tile[2] > 4096 || d.tile[0] * d.tile[1] * d.tile[2] < 32)
+      return fail(LBM_EINVAL, "tile must hold 32..4096 nodes");
+    const int n3[3] = {d.nx, d.ny, d.nz};
+    for (int a = 0; a < 3; ++a)
+      if (d.periodic[a] && n3[a] % d.tile[a])
+        return fail(LBM_EINVAL, "periodic axis %d needs extent %d divisible by the tile edge %d", a, n3[a], d.tile[a]);
+    if (nzg != d.nz) return fail(LBM_EINVAL, "tile layouts are single-slab in this build");
+  }
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (d.device < 0 || d.device >= ndev) return fail(LBM_EINVAL, "device %d not present (%d devices)", d.device, ndev);
+  DeviceGuard dg(d.device);
+  lbm_handle* h = new lbm_handle();
+  h->d = d;
+  h->d.nz_global = nzg;
+  h->esize = d.dtype == LBM_F32 ? 4 : 8;
+  Geo& g = h->g;
+  g.nx = d.nx;
+  g.ny = d.ny;
+  g.nz = d.nz;
+  g.px = d.periodic[0] != 0;
+  g.py = d.periodic[1] != 0;
+  g.pzw = (d.periodic[2] != 0) && (nzg == d.nz);
+  g.tiled = is_tiled(d.layout);
+  h->n_nodes = (long long)d.nx * d.ny * d.nz;
+  if (!g.tiled) {
+    g.nxp = (d.nx + 31) / 32 * 32;
+    g.plane = (long long)g.ny * g.nxp;
+    h->n_slots = (long long)(g.nz + 2) * g.plane;
+    g.ps = (h->n_slots + 63) / 64 * 64;
+    h->nflags = (long long)g.nz * g.plane;
+  } else {
+    g.ex = d.tile[0];
+    g.ey = d.tile[1];
+    g.ez = d.tile[2];
+    g.lex = ilog2(g.ex);
+    g.ley = ilog2(g.ey);
+    g.lez = ilog2(g.ez);
+    g.gx = (d.nx + g.ex - 1) / g.ex;
+    g.gy = (d.ny + g.ey - 1) / g.ey;
+    g.gz = (d.nz + g.ez - 1) / g.ez;
+    g.tn = g.ex * g.ey * g.ez;
+    g.nxp = d.nx;
+    h->ntiles_grid = (long long)g.gx * g.gy * g.gz;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
+  if (e == cudaSuccess) e = cudaMalloc(&h->scratch, 4096 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&h->uscratch, 4 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    lbm_destroy(h);
+    return fail(LBM_ECUDA, "stream/event setup: %s", cudaGetErrorString(e));
+  }
+  *out = h;
+  return 0;
+}
+
+void lbm_destroy(lbm_t* h) {
+  if (!h) return;
+  DeviceGuard dg(h->d.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  free_geometry(h);
+  dev_free(h->scratch);
+  dev_free(h->uscratch);
+  if (h->ev0) cudaEventDestroy(h->ev0);
+  if (h->ev1) cudaEventDestroy(h->ev1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const int32_t* bc_index,
+                     const uint8_t* ghost_lo, const uint8_t* ghost_hi, const uint8_t* bc_kind,
+                     const double* bc_vel, const double* bc_rho, int32_t nb) {
+  if (!h || !type || !orient || !bc_index) return fail(LBM_EINVAL, "NULL geometry array");
+  if (nb < 0 || nb > 255) return fail(LBM_EINVAL, "boundary table holds %d entries; at most 255 supported", nb);
+  if (nb > 0 && (!bc_kind || !bc_vel || !bc_rho)) return fail(LBM_EINVAL, "NULL boundary table");
+  DeviceGuard dg(h->d.device);
+  CK(cudaStreamSynchronize(h->stream));
+  free_geometry(h);
+  Geo& g = h->g;
+  const long long N = h->n_nodes;
+  const long long plane_nodes = (long long)g.nx * g.ny;
+  int rc = 0;
+  uint8_t *dtype_ = nullptr, *dorient = nullptr, *dglo = nullptr, *dghi = nullptr;
+  int* dbc = nullptr;
+  int* derr = nullptr;
+  int *keep = nullptr, *scan = nullptr;
+  void* cub_tmp = nullptr;
+  const int nbt = nb > 0 ? nb : 1;
+  // temporaries
+  if ((rc = dev_alloc(h, &dtype_, N)) || (rc = dev_alloc(h, &dorient, N)) ||
+      (rc = dev_alloc(h, &dbc, N * 4)) || (rc = dev_alloc(h, &derr, 16)))
+    goto done;
+  CK(cudaMemcpyAsync(dtype_, type, N, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(dorient, orient, N, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(dbc, bc_index, N * 4, cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemsetAsync(derr, 0, 16, h->stream));
+  CK(cudaMemsetAsync(h->uscratch, 0, 4 * sizeof(unsigned long long), h->stream));
+  if (ghost_lo) {
+    if ((rc = dev_alloc(h, &dglo, plane_nodes))) goto done;
+    CK(cudaMemcpyAsync(dglo, ghost_lo, plane_nodes, cudaMemcpyHostToDevice, h->stream));
+  } else if (g.pzw) {
+    dglo = nullptr;  // wrap handled below
+  }
+  if (ghost_hi) {
+    if ((rc = dev_alloc(h, &dghi, plane_nodes))) goto done;
+    CK(cudaMemcpyAsync(dghi, ghost_hi, plane_nodes, cudaMemcpyHostToDevice, h->stream));
+  }
+  {
+    // whole-domain periodic z: the ghost planes are the wrapped planes
+    const uint8_t* glo = dglo ? dglo : (g.pzw ? dtype_ + (long long)(g.nz - 1) * plane_nodes : nullptr);
+    const uint8_t* ghi = dghi ? dghi : (g.pzw ? dtype_ : nullptr);
+    // boundary tables (float64 for init, storage type for the step)
+    if ((rc = dev_alloc(h, &h->bckind64, nbt)) || (rc = dev_alloc(h, &h->bcv64, nbt * 3 * 8)) ||
+        (rc = dev_alloc(h, &h->bcr64, nbt * 8)) || (rc = dev_alloc(h, (char**)&h->bcv, nbt * 3 * h->esize)) ||
+        (rc = dev_alloc(h, (char**)&h->bcr, nbt * h->esize)))
+      goto done;
+    {
+      std::vector<uint8_t> kk(nbt, 0);
+      std::vector<double> vv(nbt * 3, 0.0), rr(nbt, 0.0);
+      for (int b = 0; b < nb; ++b) {
+        kk[b] = bc_kind[b];
+        for (int c = 0; c < 3; ++c) vv[3 * b + c] = bc_vel[3 * b + c];
+        rr[b] = bc_rho[b];
+      }
+      CK(cudaMemcpy(h->bckind64, kk.data(), nbt, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->bcv64, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(h->bcr64, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
+      if (h->esize == 4) {
+        std::vector<float> vf(nbt * 3), rf(nbt);
+        for (int k = 0; k < nbt * 3; ++k) vf[k] = (float)vv[k];
+        for (int k = 0; k < nbt; ++k) rf[k] = (float)rr[k];
+        CK(cudaMemcpy(h->bcv, vf.data(), nbt * 3 * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->bcr, rf.data(), nbt * 4, cudaMemcpyHostToDevice));
+      } else {
+        CK(cudaMemcpy(h->bcv, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->bcr, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
+      }
+    }
+    if (!g.tiled) {
+      if ((rc = dev_alloc(h, &h->flags, h->nflags * 4))) goto done;
+      dim3 grid((g.nxp + 127) / 128, g.ny, g.nz);
+      k_flags_dense<<<grid, 128, 0, h->stream>>>(h->flags, dtype_, dorient, dbc, glo, ghi, g, nb, derr,
+                                                 h->uscratch);
+      CKL();
+    } else {
+      const long long G = h->ntiles_grid;
+      if ((rc = dev_alloc(h, &h->rank, G * 4)) || (rc = dev_alloc(h, &keep, G * 4)) ||
+          (rc = dev_alloc(h, &scan, G * 4)))
+        goto done;
+      const int keep_all = h->d.layout == LBM_LAYOUT_TILE;
+      k_tile_keep<<<(unsigned)((G * 32 + 255) / 256), 256, 0, h->stream>>>(keep, dtype_, g, keep_all, G);
+      CKL();
+      size_t tmp_bytes = 0;
+      if (G > 0x7fffffffLL) { rc = fail(LBM_EINVAL, "too many tiles"); goto done; }
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, keep, scan, (int)G, h->stream));
+      if ((rc = dev_alloc(h, (char**)&cub_tmp, tmp_bytes))) goto done;
+      CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_bytes, keep, scan, (int)G, h->stream));
+      int last_scan = 0, last_keep = 0;
+      CK(cudaMemcpyAsync(&last_scan, scan + G - 1, 4, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaMemcpyAsync(&last_keep, keep + G - 1, 4, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      const long long T = (long long)last_scan + last_keep;
+      h->n_tiles = T;
+      if ((rc = dev_alloc(h, &h->tiles, (T > 0 ? T : 1) * 3 * 4)) ||
+          (rc = dev_alloc(h, &h->nbr27, (T > 0 ? T : 1) * 27 * 4)))
+        goto done;
+      k_tile_compact<<<(unsigned)((G + 255) / 256), 256, 0, h->stream>>>(h->rank, keep, scan, h->tiles, g, G);
+      CKL();
+      if (T > 0) {
+        k_tile_nbr<<<(unsigned)((T * 27 + 255) / 256), 256, 0, h->stream>>>(h->nbr27, h->tiles, h->rank, g, T);
+        CKL();
+      }
+      h->n_slots = T * g.tn;
+      g.ps = (h->n_slots + 63) / 64 * 64;
+      h->nflags = h->n_slots;
+      if ((rc = dev_alloc(h, &h->flags, (h->nflags > 0 ? h->nflags : 1) * 4))) goto done;
+      if (h->nflags > 0) {
+        k_flags_tile<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(
+            h->flags, h->tiles, dtype_, dorient, dbc, glo, ghi, g, h->nflags, nb, derr, h->uscratch);
+        CKL();
+      }
+      h->sm.rank = h->rank;
+    }
+    int herr = 0;
+    unsigned long long nons = 0;
+    CK(cudaMemcpyAsync(&herr, derr, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(&nons, h->uscratch, 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (herr & 1) { rc = fail(LBM_EINVAL, "node type or orientation out of range"); goto done; }
+    if (herr & 2) { rc = fail(LBM_EINVAL, "velocity/pressure node without a valid bc_index or orientation"); goto done; }
+    h->n_nonsolid = (long long)nons;
+    h->nb = nb;
+    // PDF buffers
+    const size_t fbytes = (size_t)Q * (size_t)(g.ps > 0 ? g.ps : 64) * h->esize;
+    if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes)) || (rc = dev_alloc(h, (char**)&h->f[1], fbytes))) goto done;
+    CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->stream));
+    CK(cudaMemsetAsync(h->f[1], 0, fbytes, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->geometry = true;
+    h->parity = 0;
+    h->step_count = h->visited_total = 0;
+  }
+done:
+  {
+    cudaStreamSynchronize(h->stream);
+    dev_free(dtype_);
+    dev_free(dorient);
+    dev_free(dbc);
+    dev_free(dglo);
+    dev_free(dghi);
+    dev_free(derr);
+    dev_free(keep);
+    dev_free(scan);
+    dev_free(cub_tmp);
+    // recompute resident bytes (temporaries released)
+    if (h->geometry) {
+      long long b = 2LL * Q * (h->g.ps > 0 ? h->g.ps : 64) * h->esize + h->nflags * 4;
+      if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * 30 * 4;
+      h->device_bytes = b;
+    }
+  }
+  if (rc) free_geometry(h);
+  return rc;
+}
+
+int lbm_init_equilibrium(lbm_t* h, const double* rho, const double* ux, const double* uy,
+                         const double* uz, double rho0, double ux0, double uy0, double uz0) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_init_equilibrium");
+  DeviceGuard dg(h->d.device);
+  const Geo& g = h->g;
+  const long long N = h->n_nodes;
+  const double* src[4] = {rho, ux, uy, uz};
+  double* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int rc = 0;
+  for (int k = 0; k < 4 && !rc; ++k) {
+    if (!src[k]) continue;
+    cudaError_t e = cudaMalloc(&dev[k], N * 8);
+    if (e != cudaSuccess) {
+      rc = fail(LBM_ENOMEM, "init field upload: %s", cudaGetErrorString(e));
+      break;
+    }
+    e = cudaMemcpyAsync(dev[k], src[k], N * 8, cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) rc = fail(LBM_ECUDA, "init upload: %s", cudaGetErrorString(e));
+  }
+  if (!rc) {
+    const size_t fbytes = (size_t)Q * g.ps * h->esize;
+    cudaMemsetAsync(h->f[0], 0, fbytes, h->stream);
+    cudaMemsetAsync(h->f[1], 0, fbytes, h->stream);
+    h->parity = 0;
+    const int bx = 128;
+    if (h->esize == 4)
+      k_init<float><<<node_grid(g, bx), bx, 0, h->stream>>>((float*)h->f[0], h->flags, h->sm, g, dev[0], dev[1],
+                                                            dev[2], dev[3], rho0, ux0, uy0, uz0, h->bckind64,
+                                                            h->bcv64, h->bcr64, h->nb);
+    else
+      k_init<double><<<node_grid(g, bx), bx, 0, h->stream>>>((double*)h->f[0], h->flags, h->sm, g, dev[0], dev[1],
+                                                             dev[2], dev[3], rho0, ux0, uy0, uz0, h->bckind64,
+                                                             h->bcv64, h->bcr64, h->nb);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) rc = fail(LBM_ECUDA, "k_init: %s", cudaGetErrorString(e));
+  }
+  for (int k = 0; k < 4; ++k) dev_free(dev[k]);
+  if (rc) return rc;
+  h->initialized = true;
+  h->step_count = h->visited_total = 0;
+  return 0;
+}
+
+int lbm_set_omega(lbm_t* h, double omega) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!(omega > 0.0 && omega < 2.0)) return fail(LBM_EINVAL, "omega must lie in (0, 2), got %g", omega);
+  h->d.omega = omega;
+  return 0;
+}
+
+int lbm_step(lbm_t* h, int64_t n) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (n < 0) return fail(LBM_EINVAL, "n_steps must be >= 0, got %lld", (long long)n);
+  if (!h->initialized) return fail(LBM_ESTATE, "initialize() must run before stepping");
+  DeviceGuard dg(h->d.device);
+  CK(cudaEventRecord(h->ev0, h->stream));
+  for (int64_t k = 0; k < n; ++k) {
+    const void* pre = h->f[h->parity];
+    void* post = h->f[1 - h->parity];
+    if (h->esize == 4)
+      launch_step<float>(h, pre, post);
+    else
+      launch_step<double>(h, pre, post);
+    h->parity ^= 1;
+  }
+  CKL();
+  CK(cudaEventRecord(h->ev1, h->stream));
+  CK(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  h->last_ms = ms;
+  h->step_count += n;
+  const long long visits = (h->d.layout == LBM_LAYOUT_DENSE) ? h->n_nodes
+                           : (h->d.layout == LBM_LAYOUT_BITMASK_NODE) ? h->n_nonsolid
+                                                                       : h->n_slots;
+  h->visited_total += n * visits;
+  return 0;
+}
+
+int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  const long long N = h->n_nodes;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, N * 8 * 4);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "macroscopic readback: %s", cudaGetErrorString(e));
+  const int bx = 128;
+  const Geo& g = h->g;
+  double *r = d, *a = d + N, *b = d + 2 * N, *c = d + 3 * N;
+  if (h->esize == 4)
+    k_macro<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->sm, g, r, a, b, c);
+  else
+    k_macro<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->sm, g, r, a, b, c);
+  e = cudaGetLastError();
+  double* outs[4] = {rho, ux, uy, uz};
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    if (outs[k]) e = cudaMemcpyAsync(outs[k], d + k * N, N * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "macroscopic: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  const Geo& g = h->g;
+  const unsigned long long none = ~0ULL;
+  const long long V = g.tiled ? h->n_slots : h->n_nodes;
+  CK(cudaMemcpyAsync(h->uscratch, &none, 8, cudaMemcpyHostToDevice, h->stream));
+  const int bx = 128;
+  if (h->esize == 4)
+    k_nonfinite<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->sm, g, V, h->uscratch);
+  else
+    k_nonfinite<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->sm, g, V, h->uscratch);
+  CKL();
+  unsigned long long best = 0;
+  CK(cudaMemcpyAsync(&best, h->uscratch, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (best == none) {
+    if (dir) *dir = -1;
+    return 0;
+  }
+  const long long i = (long long)(best / (unsigned long long)V);
+  const long long v = (long long)(best % (unsigned long long)V);
+  int x, y, z;
+  if (!g.tiled) {
+    x = (int)(v % g.nx);
+    y = (int)((v / g.nx) % g.ny);
+    z = (int)(v / ((long long)g.nx * g.ny));
+  } else {
+    const long long t = v / g.tn;
+    const int l = (int)(v % g.tn);
+    int tc[3];
+    CK(cudaMemcpy(tc, h->tiles + 3 * t, 12, cudaMemcpyDeviceToHost));
+    x = tc[0] * g.ex + (l & (g.ex - 1));
+    y = tc[1] * g.ey + ((l >> g.lex) & (g.ey - 1));
+    z = tc[2] * g.ez + (l >> (g.lex + g.ley));
+  }
+  if (dir) *dir = (int32_t)i;
+  if (node_xyz) {
+    node_xyz[0] = x;
+    node_xyz[1] = y;
+    node_xyz[2] = z;
+  }
+  return fail(LBM_EDIVERGED, "non-finite distribution at node (%d, %d, %d), direction %lld", x, y, z, i);
+}
+
+int lbm_total_mass(lbm_t* h, double* mass) {
+  if (!h || !mass) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  const int nblk = 1184;  // 8 x 148 SMs; fixed so the reduction order is fixed
+  if (h->esize == 4)
+    k_mass_partial<float><<<nblk, 256, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->g, h->nflags, h->scratch);
+  else
+    k_mass_partial<double><<<nblk, 256, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->g, h->nflags, h->scratch);
+  k_mass_final<<<1, 256, 0, h->stream>>>(h->scratch, nblk, h->scratch + nblk);
+  CKL();
+  CK(cudaMemcpyAsync(mass, h->scratch + nblk, 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+static int pdf_io(lbm_t* h, int which, void* host, bool get) {
+  if (!h || !host) return fail(LBM_EINVAL, "NULL argument");
+  if (which != 0 && which != 1) return fail(LBM_EINVAL, "which must be 0 (pre) or 1 (post)");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  const long long bytes = (long long)Q * h->n_nodes * h->esize;
+  void* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, bytes);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "pdf staging: %s", cudaGetErrorString(e));
+  void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
+  const Geo& g = h->g;
+  const int bx = 128;
+  if (get) {
+    if (h->esize == 4)
+      k_get_pdf<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)buf, h->sm, g, (float*)d);
+    else
+      k_get_pdf<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)buf, h->sm, g, (double*)d);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, d, bytes, cudaMemcpyDeviceToHost, h->stream);
+  } else {
+    e = cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) {
+      if (h->esize == 4)
+        k_set_pdf<float><<<node_grid(g, bx), bx, 0, h->stream>>>((float*)buf, h->sm, g, (const float*)d);
+      else
+        k_set_pdf<double><<<node_grid(g, bx), bx, 0, h->stream>>>((double*)buf, h->sm, g, (const double*)d);
+      e = cudaGetLastError();
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "pdf io: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int lbm_get_pdf(lbm_t* h, int32_t which, void* out) { return pdf_io(h, which, out, true); }
+int lbm_set_pdf(lbm_t* h, int32_t which, const void* in) { return pdf_io(h, which, (void*)in, false); }
+
+static int field_io(lbm_t* h, int which, void* host, bool get) {
+  if (!h || !host) return fail(LBM_EINVAL, "NULL argument");
+  if (which != 0 && which != 1) return fail(LBM_EINVAL, "which must be 0 (pre) or 1 (post)");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
+  const size_t bytes = (size_t)Q * h->g.ps * h->esize;
+  if (get)
+    CK(cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost));
+  else
+    CK(cudaMemcpy(buf, host, bytes, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int lbm_get_field(lbm_t* h, int32_t which, void* out) { return field_io(h, which, out, true); }
+int lbm_set_field(lbm_t* h, int32_t which, const void* in) { return field_io(h, which, (void*)in, false); }
+
+int lbm_get_slot_of(lbm_t* h, int32_t* out) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  int* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, h->n_nodes * 4);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "slot_of staging: %s", cudaGetErrorString(e));
+  k_slot_of<<<node_grid(h->g, 128), 128, 0, h->stream>>>(h->sm, h->g, d);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, h->n_nodes * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "slot_of: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int lbm_get_flags(lbm_t* h, uint32_t* out) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  DeviceGuard dg(h->d.device);
+  uint32_t* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, h->n_nodes * 4);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "flags staging: %s", cudaGetErrorString(e));
+  k_get_flags<<<node_grid(h->g, 128), 128, 0, h->stream>>>(h->flags, h->sm, h->g, d);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, h->n_nodes * 4, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "flags: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int lbm_get_tile_index(lbm_t* h, int32_t* tiles, int32_t* nbr27, int64_t* n_tiles) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  if (n_tiles) *n_tiles = h->n_tiles;
+  if (!h->g.tiled) return 0;
+  DeviceGuard dg(h->d.device);
+  if (tiles && h->n_tiles) CK(cudaMemcpy(tiles, h->tiles, h->n_tiles * 12, cudaMemcpyDeviceToHost));
+  if (nbr27 && h->n_tiles) CK(cudaMemcpy(nbr27, h->nbr27, h->n_tiles * 27 * 4, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int lbm_get_stats(lbm_t* h, lbm_stats* s) {
+  if (!h || !s) return fail(LBM_EINVAL, "NULL argument");
+  memset(s, 0, sizeof(*s));
+  s->n_nodes = h->n_nodes;
+  s->n_nonsolid = h->n_nonsolid;
+  s->visits_per_step = (h->d.layout == LBM_LAYOUT_DENSE) ? h->n_nodes
+                       : (h->d.layout == LBM_LAYOUT_BITMASK_NODE) ? h->n_nonsolid
+                                                                   : h->n_slots;
+  s->n_slots = h->n_slots;
+  s->plane_stride = h->g.ps;
+  s->n_tiles = h->n_tiles;
+  s->step_count = h->step_count;
+  s->visited_nodes_total = h->visited_total;
+  s->device_bytes = h->device_bytes;
+  s->launches_total = h->launches;
+  s->last_step_ms = h->last_ms;
+  s->parity = h->parity;
+  s->initialized = h->initialized ? 1 : 0;
+  return 0;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- scalar host math
+template <typename T>
+static void to_t(const double* in, T* out, int n) {
+  for (int k = 0; k < n; ++k) out[k] = (T)in[k];
+}
+template <typename T>
+static void from_t(const T* in, double* out, int n) {
+  for (int k = 0; k < n; ++k) out[k] = (double)in[k];
+}
+
+template <typename T>
+static int feq_t(double rho, const double* u3, double* out) {
+  T e[Q];
+  feq19<T>((T)rho, (T)u3[0], (T)u3[1], (T)u3[2], e);
+  from_t(e, out, Q);
+  return 0;
+}
+
+extern "C" int lbm19_feq(int32_t dtype, double rho, const double* u3, double* out19) {
+  if (!u3 || !out19) return fail(LBM_EINVAL, "NULL argument");
+  return dtype == LBM_F32 ? feq_t<float>(rho, u3, out19) : feq_t<double>(rho, u3, out19);
+}
+
+template <typename T>
+static int moments_t(const double* f19, double* rho, double* u3) {
+  T f[Q], r, a, b, c;
+  to_t(f19, f, Q);
+  moments19<T>(f, r, a, b, c);
+  *rho = r;
+  u3[0] = a;
+  u3[1] = b;
+  u3[2] = c;
+  return 0;
+}
+
+extern "C" int lbm19_moments(int32_t dtype, const double* f19, double* rho, double* u3) {
+  if (!f19 || !rho || !u3) return fail(LBM_EINVAL, "NULL argument");
+  return dtype == LBM_F32 ? moments_t<float>(f19, rho, u3) : moments_t<double>(f19, rho, u3);
+}
+
+template <typename T>
+static int collide_t(const double* f19, double omega, double* out) {
+  T f[Q], r, a, b, c;
+  to_t(f19, f, Q);
+  moments19<T>(f, r, a, b, c);
+  collide19<T>(f, r, a, b, c, (T)omega);
+  from_t(f, out, Q);
+  return 0;
+}
+
+extern "C" int lbm19_collide(int32_t dtype, const double* f19, double omega, double* out19) {
+  if (!f19 || !out19) return fail(LBM_EINVAL, "NULL argument");
+  return dtype == LBM_F32 ? collide_t<float>(f19, omega, out19) : collide_t<double>(f19, omega, out19);
+}
+
+template <typename T>
+static int zhv_t(const double* f19, int orient, const double* u3, double* out) {
+  T f[Q];
+  to_t(f19, f, Q);
+  zou_he_velocity19<T>(f, (uint32_t)orient, (T)u3[0], (T)u3[1], (T)u3[2]);
+  from_t(f, out, Q);
+  return 0;
+}
+
+extern "C" int lbm19_zou_he_velocity(int32_t dtype, const double* f19, int32_t orient, const double* u3, double* out19) {
+  if (!f19 || !u3 || !out19) return fail(LBM_EINVAL, "NULL argument");
+  if (orient < O_NORTH || orient > O_BOTTOM) return fail(LBM_EINVAL, "orientation must name a face, got %d", orient);
+  return dtype == LBM_F32 ? zhv_t<float>(f19, orient, u3, out19) : zhv_t<double>(f19, orient, u3, out19);
+}
+
+template <typename T>
+static int zhp_t(const double* f19, int orient, double rw, double* out) {
+  T f[Q];
+  to_t(f19, f, Q);
+  zou_he_pressure19<T>(f, (uint32_t)orient, (T)rw);
+  from_t(f, out, Q);
+  return 0;
+}
+
+extern "C" int lbm19_zou_he_pressure(int32_t dtype, const double* f19, int32_t orient, double rho_wall, double* out19) {
+  if (!f19 || !out19) return fail(LBM_EINVAL, "NULL argument");
+  if (orient < O_NORTH || orient > O_BOTTOM) return fail(LBM_EINVAL, "orientation must name a face, got %d", orient);
+  return dtype == LBM_F32 ? zhp_t<float>(f19, orient, rho_wall, out19) : zhp_t<double>(f19, orient, rho_wall, out19);
+}
+
+
