@@ -1,0 +1,17 @@
+#!/bin/bash
+# ncu evidence for the step kernels (run under gpurun, one GPU):
+#   1. launch list with device times (cold-cache, serialised: compare shares)
+#   2. one `--set full` capture of the step kernel per workload
+# usage: bash profiles/profile.sh <tag> [workload ...]
+set -u
+TAG=${1:-r01}; shift || true
+WLS=${@:-channel512}
+mkdir -p gpurun_out
+for W in $WLS; do
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
+      --log-file gpurun_out/launches_${TAG}_${W}.csv \
+      python bench.py --workload $W --steps 5 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 \
+      -o gpurun_out/prof_${TAG}_${W} -f \
+      python bench.py --workload $W --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_${TAG}_${W}.log 2>&1
+done

@@ -188,7 +188,7 @@ def test_run_observers_and_counters():
     assert calls == list(range(10, 101, 10))
     assert sim.step_count == 100
     assert sim.visited_nodes_total == 100 * 16 * 16 * 8
-    with pytest.raises(RuntimeError, match="observer failed at step 3"):
+    with pytest.raises(RuntimeError, match="observer failed at step 102"):
         sim.run(5, observers=[(3, lambda *a: (_ for _ in ()).throw(KeyError("x")))])
 
 
