@@ -390,10 +390,18 @@ __device__ __forceinline__ bool sector_needs_zero(bool nonsolid) {
   return (act & grp) != 0u;
 }
 
+// 19 direction planes of one buffer, resolved on the host once per launch, so
+// every access is a 32-bit slot offset from a per-direction base pointer
+template <typename T>
+struct Planes {
+  const T* pre[Q];
+  T* post[Q];
+};
+
 template <typename T>
 __device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
                                                  const T* __restrict__ bcr, T om,
-                                                 T* __restrict__ post, long long ps, long long s) {
+                                                 const Planes<T>& P, int s) {
   const uint32_t t = flag_type(w);
   if (t == VELOCITY_BC) {
     const uint32_t b = flag_bc(w);
@@ -405,12 +413,30 @@ __device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T*
   moments19(f, rho, vx, vy, vz);
   collide19(f, rho, vx, vy, vz, om);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) post[(long long)i * ps + s] = f[i];
+  for (int i = 0; i < Q; ++i) P.post[i][s] = f[i];
+}
+
+// Link-wise bounce-back fix-up: every f_i was loaded speculatively from the
+// upstream slot (always a valid address); where the mask bit of opp(i) is
+// clear the node reflects its own f_opp(i) instead (reference kernel.py:84-116).
+template <typename T>
+__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t w, const Planes<T>& P, int s) {
+  const uint32_t miss = ~w & kMaskBits;
+  if (miss) {
+#pragma unroll
+    for (int i = 1; i < Q; ++i)
+      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(P.pre[opp(i)] + s);
+  }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_step_dense(const T* __restrict__ pre, T* __restrict__ post,
-                                                   const uint32_t* __restrict__ flags,
+__device__ __forceinline__ void zero_fill(const Planes<T>& P, int s) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) P.post[i][s] = (T)0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
                                                    const T* __restrict__ bcv,
                                                    const T* __restrict__ bcr, Geo g, T om) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -418,17 +444,15 @@ __global__ void __launch_bounds__(128) k_step_dense(const T* __restrict__ pre, T
   if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
   const int fi = (z * g.ny + y) * g.nxp + x;
   const int s = fi + (int)g.plane;
-  const uint32_t w = flags[fi];
+  const uint32_t w = __ldg(flags + fi);
   const bool live = flag_type(w) != SOLID;
   const bool zfill = sector_needs_zero<T>(live);
   if (!live) {
-    if (zfill) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) post[(long long)i * g.ps + s] = (T)0;
-    }
+    if (zfill) zero_fill(P, s);
     return;
   }
-  // offsets to the upstream node x - c_i along each axis (wrap on periodic axes)
+  // offsets to the upstream node x - c_i along each axis (wrap on periodic
+  // axes; on closed axes the edge offset is 0 and the fix-up replaces it)
   const int xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
   const int xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
   const int ym = y == 0 ? (g.py ? (g.ny - 1) * g.nxp : 0) : -g.nxp;
@@ -437,62 +461,66 @@ __global__ void __launch_bounds__(128) k_step_dense(const T* __restrict__ pre, T
   const int zm = (z == 0 && g.pzw) ? (g.nz - 1) * pl : -pl;
   const int zp = (z == g.nz - 1 && g.pzw) ? -(g.nz - 1) * pl : pl;
   T f[Q];
-  f[0] = __ldg(pre + s);
+  f[0] = __ldg(P.pre[0] + s);
 #pragma unroll
   for (int i = 1; i < Q; ++i) {
-    const int o = opp(i);
     const int off = (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0)) +
                     (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0)) +
                     (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0));
-    const bool present = (w >> (o - 1)) & 1u;
-    const T* src = present ? pre + (long long)i * g.ps + (s + off) : pre + (long long)o * g.ps + s;
-    f[i] = __ldg(src);
+    f[i] = __ldg(P.pre[i] + (s + off));
   }
-  bc_collide_store<T>(f, w, bcv, bcr, om, post, g.ps, s);
+  bounce_back_fixup(f, w, P, s);
+  bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
 }
 
+// Sparse tiles: one CTA per kept tile.  The upstream slot of direction i is
+// separable per axis: tile code (dx+1) + 3(dy+1) + 9(dz+1) into nbr27 and the
+// in-tile offset lx' + ex ly' + ex ey lz', each from a per-thread table.
 template <typename T>
-__global__ void k_step_tile(const T* __restrict__ pre, T* __restrict__ post,
-                            const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
-                            const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om) {
+__global__ void __launch_bounds__(256) k_step_tile(const Planes<T> P, const uint32_t* __restrict__ flags,
+                                                  const int* __restrict__ nbr27,
+                                                  const T* __restrict__ bcv, const T* __restrict__ bcr,
+                                                  Geo g, T om) {
   __shared__ int snbr[27];
   const int t = blockIdx.x;
-  if (threadIdx.x < 27) snbr[threadIdx.x] = nbr27[27LL * t + threadIdx.x];
+  if (threadIdx.x < 27) {
+    const int v = nbr27[27LL * t + threadIdx.x];
+    snbr[threadIdx.x] = v < 0 ? t : v;  // absent tiles: links are masked, read own tile
+  }
   __syncthreads();
+  const int exy = g.ex * g.ey;
   for (int l = threadIdx.x; l < g.tn; l += blockDim.x) {
-    const long long s = (long long)t * g.tn + l;
-    const uint32_t w = flags[s];
+    const int s = t * g.tn + l;
+    const uint32_t w = __ldg(flags + s);
     const bool live = flag_type(w) != SOLID;
-    const bool z0 = sector_needs_zero<T>(live);
+    const bool zfill = sector_needs_zero<T>(live);
     if (!live) {
-      if (z0) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) post[(long long)i * g.ps + s] = (T)0;
-      }
+      if (zfill) zero_fill(P, s);
       continue;
     }
     const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
+    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, local offset)
+    const int cxm = lx == 0 ? -1 : 0, lxm = lx == 0 ? g.ex - 1 : lx - 1;
+    const int cxp = lx == g.ex - 1 ? 1 : 0, lxp = lx == g.ex - 1 ? 0 : lx + 1;
+    const int cym = ly == 0 ? -3 : 0, lym = (ly == 0 ? g.ey - 1 : ly - 1) * g.ex;
+    const int cyp = ly == g.ey - 1 ? 3 : 0, lyp = (ly == g.ey - 1 ? 0 : ly + 1) * g.ex;
+    const int czm = lz == 0 ? -9 : 0, lzm = (lz == 0 ? g.ez - 1 : lz - 1) * exy;
+    const int czp = lz == g.ez - 1 ? 9 : 0, lzp = (lz == g.ez - 1 ? 0 : lz + 1) * exy;
+    const int ly0 = ly * g.ex, lz0 = lz * exy;
     T f[Q];
-    f[0] = __ldg(pre + s);
+    f[0] = __ldg(P.pre[0] + s);
 #pragma unroll
     for (int i = 1; i < Q; ++i) {
-      const int o = opp(i);
-      const bool present = (w >> (o - 1)) & 1u;
-      long long idx;
-      if (present) {
-        const int sx = lx - cx(i), sy = ly - cy(i), sz = lz - cz(i);
-        const int dx = sx < 0 ? -1 : (sx >= g.ex ? 1 : 0);
-        const int dy = sy < 0 ? -1 : (sy >= g.ey ? 1 : 0);
-        const int dz = sz < 0 ? -1 : (sz >= g.ez ? 1 : 0);
-        const int nt = snbr[(dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)];
-        const int sl = (((sz & (g.ez - 1)) << g.ley) + (sy & (g.ey - 1))) << g.lex | (sx & (g.ex - 1));
-        idx = (long long)i * g.ps + (long long)nt * g.tn + sl;
-      } else {
-        idx = (long long)o * g.ps + s;
-      }
-      f[i] = __ldg(pre + idx);
+      const int code = 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) +
+                       (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
+                       (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
+      const int loc = (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx)) +
+                      (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
+                      (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
+      f[i] = __ldg(P.pre[i] + (snbr[code] * g.tn + loc));
     }
-    bc_collide_store<T>(f, w, bcv, bcr, om, post, g.ps, s);
+    bounce_back_fixup(f, w, P, s);
+    bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
   }
 }
 
@@ -594,16 +622,20 @@ template <typename T>
 int launch_step(lbm_handle* h, const void* pre, void* post) {
   const Geo& g = h->g;
   const T om = (T)h->d.omega;
+  Planes<T> P;
+  for (int i = 0; i < Q; ++i) {
+    P.pre[i] = (const T*)pre + (size_t)i * g.ps;
+    P.post[i] = (T*)post + (size_t)i * g.ps;
+  }
   if (!g.tiled) {
     const int bx = 128;
     dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
-    k_step_dense<T><<<grid, bx, 0, h->stream>>>((const T*)pre, (T*)post, h->flags,
-                                                 (const T*)h->bcv, (const T*)h->bcr, g, om);
+    k_step_dense<T><<<grid, bx, 0, h->stream>>>(P, h->flags, (const T*)h->bcv, (const T*)h->bcr, g, om);
   } else {
     if (h->n_tiles == 0) return 0;
-    const int bt = g.tn < 512 ? g.tn : 512;
-    k_step_tile<T><<<(unsigned)h->n_tiles, bt, 0, h->stream>>>(
-        (const T*)pre, (T*)post, h->flags, h->nbr27, (const T*)h->bcv, (const T*)h->bcr, g, om);
+    const int bt = g.tn < 256 ? g.tn : 256;
+    k_step_tile<T><<<(unsigned)h->n_tiles, bt, 0, h->stream>>>(P, h->flags, h->nbr27, (const T*)h->bcv,
+                                                                (const T*)h->bcr, g, om);
   }
   h->launches += 1;
   return 0;
@@ -804,6 +836,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       CK(cudaMemcpyAsync(&last_keep, keep + G - 1, 4, cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));
       const long long T = (long long)last_scan + last_keep;
+      if (T * g.tn >= (1LL << 31)) { rc = fail(LBM_EINVAL, "%lld kept tiles exceed 2^31 slots", T); goto done; }
       h->n_tiles = T;
       if ((rc = dev_alloc(h, &h->tiles, (T > 0 ? T : 1) * 3 * 4)) ||
           (rc = dev_alloc(h, &h->nbr27, (T > 0 ? T : 1) * 27 * 4)))
