@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variants", default=None,
+                    help="comma list of step-kernel variants to time in-process (tuning)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -242,6 +244,22 @@ def main():
     import paper_2108_13241_b200 as lb
     workload = args.workload or "channel512"
     geom, params, layout, desc, rho0 = build_workload(workload)
+    if args.variants:
+        for v in args.variants.split(","):
+            os.environ["LBM_STEP_VARIANT"] = v
+            sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
+            sim.initialize(rho0)
+            sim.step(args.warmup)
+            sim.step(args.steps)
+            ms = sim.last_step_ms
+            nons = sim.active_node_count
+            mlups = nons * args.steps / (ms / 1e3) / 1e6
+            peak, _ = measured_peak()
+            frac = nons * BYTES_PER_NODE_F32 / (ms / args.steps / 1e3) / 1e9 / peak
+            print(json.dumps({"workload": workload, "variant": v, "mlups": round(mlups),
+                              "frac": round(frac, 4), "ms_per_step": ms / args.steps}), flush=True)
+            sim.close()
+        return
     sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
     sim.initialize(rho0)
     sim.step(args.warmup)

@@ -132,7 +132,8 @@ int lbm_total_mass(lbm_t* h, double* mass);
  * nodes without storage read 0 (set_pdf ignores them). */
 int lbm_get_pdf(lbm_t* h, int32_t which, void* out);
 int lbm_set_pdf(lbm_t* h, int32_t which, const void* in);
-/* Native storage: (19, plane_stride) in the handle dtype. */
+/* Native storage, 19 * plane_stride elements in the handle dtype: dense
+ * (19, plane_stride) SoA; tile layouts AoSoA (n_tiles, 19, tile nodes). */
 int lbm_get_field(lbm_t* h, int32_t which, void* out);
 int lbm_set_field(lbm_t* h, int32_t which, const void* in);
 /* slot of each node (nz, ny, nx), -1 when the node has no storage. */

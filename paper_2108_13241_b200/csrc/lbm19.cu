@@ -27,6 +27,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,7 +75,16 @@ struct Geo {
   int ex, ey, ez, lex, ley, lez;  // tile edges and their log2
   int gx, gy, gz;          // tile grid
   int tn;                  // nodes per tile
+  int ltn;                 // log2(tn)
+  int zero_fill;           // complete mixed sectors with zeros (full-sector stores)
 };
+
+// element index of (direction i, slot s): dense SoA i*ps + s; tiles AoSoA
+// f[tile][i][node], i.e. each tile's 19 direction blocks are contiguous
+__device__ __forceinline__ long long fidx(const Geo& g, int i, long long s) {
+  if (!g.tiled) return (long long)i * g.ps + s;
+  return ((s >> g.ltn) * Q + i) << g.ltn | (s & (g.tn - 1));
+}
 
 struct SlotMap {
   const int* rank;  // tile rank grid (gz, gy, gx), -1 = not allocated (tile layouts)
@@ -248,7 +258,7 @@ __global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, 
     r = bcr[b];
   }
 #pragma unroll
-  for (int i = 0; i < Q; ++i) pre[(long long)i * g.ps + s] = (T)init_eq(i, r, vx, vy, vz);
+  for (int i = 0; i < Q; ++i) pre[fidx(g, i, s)] = (T)init_eq(i, r, vx, vy, vz);
 }
 
 template <typename T>
@@ -264,7 +274,7 @@ __global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ 
   if (s >= 0 && flag_type(flags[sm.flag_index(g, s)]) != SOLID) {
     double f[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = (double)pre[(long long)i * g.ps + s];
+    for (int i = 0; i < Q; ++i) f[i] = (double)pre[fidx(g, i, s)];
     using A = ar<double>;
     r = density19(f);
     if (r != 0.0) {
@@ -290,7 +300,7 @@ __global__ void k_get_pdf(const T* __restrict__ buf, SlotMap sm, Geo g, T* __res
   const long long n = ((long long)z * g.ny + y) * g.nx + x;
   const long long s = sm.slot(g, x, y, z);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) out[i * N + n] = s >= 0 ? buf[(long long)i * g.ps + s] : (T)0;
+  for (int i = 0; i < Q; ++i) out[i * N + n] = s >= 0 ? buf[fidx(g, i, s)] : (T)0;
 }
 
 template <typename T>
@@ -303,7 +313,7 @@ __global__ void k_set_pdf(T* __restrict__ buf, SlotMap sm, Geo g, const T* __res
   const long long s = sm.slot(g, x, y, z);
   if (s < 0) return;
 #pragma unroll
-  for (int i = 0; i < Q; ++i) buf[(long long)i * g.ps + s] = in[i * N + n];
+  for (int i = 0; i < Q; ++i) buf[fidx(g, i, s)] = in[i * N + n];
 }
 
 __global__ void k_slot_of(SlotMap sm, Geo g, int* __restrict__ out) {
@@ -334,7 +344,7 @@ __global__ void k_nonfinite(const T* __restrict__ pre, const uint32_t* __restric
   if (s < 0 || flag_type(flags[sm.flag_index(g, s)]) == SOLID) return;
   const long long v = g.tiled ? s : ((long long)z * g.ny + y) * g.nx + x;
   for (int i = 0; i < Q; ++i) {
-    const T val = pre[(long long)i * g.ps + s];
+    const T val = pre[fidx(g, i, s)];
     if (!isfinite((double)val)) {
       atomicMin(best, (unsigned long long)(i * V + v));
       return;
@@ -353,7 +363,7 @@ __global__ void k_mass_partial(const T* __restrict__ pre, const uint32_t* __rest
     if (flag_type(flags[k]) == SOLID) continue;
     const long long s = g.tiled ? k : k + g.plane;
     double a = 0.0;
-    for (int i = 0; i < Q; ++i) a += (double)pre[(long long)i * g.ps + s];
+    for (int i = 0; i < Q; ++i) a += (double)pre[fidx(g, i, s)];
     acc += a;
   }
   sh[threadIdx.x] = acc;
@@ -420,12 +430,29 @@ __device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T*
 // upstream slot (always a valid address); where the mask bit of opp(i) is
 // clear the node reflects its own f_opp(i) instead (reference kernel.py:84-116).
 template <typename T>
-__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t w, const Planes<T>& P, int s) {
-  const uint32_t miss = ~w & kMaskBits;
+__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, const Planes<T>& P, int s) {
   if (miss) {
 #pragma unroll
     for (int i = 1; i < Q; ++i)
       if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(P.pre[opp(i)] + s);
+  }
+}
+
+// Gather of the 18 moving populations.  MODE 0: speculative pull of every
+// upstream slot, then the fix-up for masked links.  MODE 1: warps whose live
+// nodes all have full masks pull unconditionally, the others select per link
+// so no byte is fetched for a masked link.
+template <typename T, int MODE, typename Up>
+__device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, const Planes<T>& P, int s,
+                                       Up up) {
+  if (MODE == 0 || fast) {
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = __ldg(P.pre[i] + up(i));
+    if (MODE == 0) bounce_back_fixup(f, miss, P, s);
+  } else {
+#pragma unroll
+    for (int i = 1; i < Q; ++i)
+      f[i] = ((miss >> (opp(i) - 1)) & 1u) ? __ldg(P.pre[opp(i)] + s) : __ldg(P.pre[i] + up(i));
   }
 }
 
@@ -435,8 +462,8 @@ __device__ __forceinline__ void zero_fill(const Planes<T>& P, int s) {
   for (int i = 0; i < Q; ++i) P.post[i][s] = (T)0;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
+template <typename T, int MODE, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
                                                    const T* __restrict__ bcv,
                                                    const T* __restrict__ bcr, Geo g, T om) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -446,13 +473,17 @@ __global__ void __launch_bounds__(128) k_step_dense(const Planes<T> P, const uin
   const int s = fi + (int)g.plane;
   const uint32_t w = __ldg(flags + fi);
   const bool live = flag_type(w) != SOLID;
-  const bool zfill = sector_needs_zero<T>(live);
+  const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+  const uint32_t miss = ~w & kMaskBits;
+  // warps whose live nodes all have full masks pull unconditionally; the
+  // rest select per link, so no byte is fetched for a masked link
+  const bool fast = MODE == 1 && __all_sync(0xffffffffu, !live || miss == 0u);
   if (!live) {
     if (zfill) zero_fill(P, s);
     return;
   }
   // offsets to the upstream node x - c_i along each axis (wrap on periodic
-  // axes; on closed axes the edge offset is 0 and the fix-up replaces it)
+  // axes; on closed axes the edge offset is 0 and the link is masked)
   const int xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
   const int xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
   const int ym = y == 0 ? (g.py ? (g.ny - 1) * g.nxp : 0) : -g.nxp;
@@ -460,46 +491,53 @@ __global__ void __launch_bounds__(128) k_step_dense(const Planes<T> P, const uin
   const int pl = (int)g.plane;
   const int zm = (z == 0 && g.pzw) ? (g.nz - 1) * pl : -pl;
   const int zp = (z == g.nz - 1 && g.pzw) ? -(g.nz - 1) * pl : pl;
+  auto up = [&](int i) {
+    return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0)) +
+           (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0));
+  };
   T f[Q];
   f[0] = __ldg(P.pre[0] + s);
-#pragma unroll
-  for (int i = 1; i < Q; ++i) {
-    const int off = (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0)) +
-                    (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0)) +
-                    (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0));
-    f[i] = __ldg(P.pre[i] + (s + off));
-  }
-  bounce_back_fixup(f, w, P, s);
+  gather<T, MODE>(f, miss, fast, P, s, up);
   bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
 }
 
-// Sparse tiles: one CTA per kept tile.  The upstream slot of direction i is
-// separable per axis: tile code (dx+1) + 3(dy+1) + 9(dz+1) into nbr27 and the
-// in-tile offset lx' + ex ly' + ex ey lz', each from a per-thread table.
-template <typename T>
-__global__ void __launch_bounds__(256) k_step_tile(const Planes<T> P, const uint32_t* __restrict__ flags,
-                                                  const int* __restrict__ nbr27,
-                                                  const T* __restrict__ bcv, const T* __restrict__ bcr,
-                                                  Geo g, T om) {
-  __shared__ int snbr[27];
+// Sparse tiles, AoSoA storage f[tile][i][TN]: one CTA per kept tile.  All
+// addresses are 32-bit element offsets from the CTA's own tile block; the
+// upstream slot of direction i is separable per axis (tile code
+// (dx+1) + 3(dy+1) + 9(dz+1), relative tile offset from shared memory, and
+// in-tile offset lx' + ex ly' + ex ey lz'), and every own-tile access
+// (bounce-back, stores) has a compile-time offset i*TN.
+// MODE 0: speculative pull + fix-up; MODE 1: select per link (no masked
+// link fetches a byte).
+template <typename T, int TN, int MODE, int MINB>
+__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
+k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
+             const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  __shared__ int srel[27];
   const int t = blockIdx.x;
   if (threadIdx.x < 27) {
-    const int v = nbr27[27LL * t + threadIdx.x];
-    snbr[threadIdx.x] = v < 0 ? t : v;  // absent tiles: links are masked, read own tile
+    const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
+    srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);  // absent: masked links, own tile
   }
   __syncthreads();
+  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
+  T* __restrict__ tp = post + (size_t)t * (Q * TN);
   const int exy = g.ex * g.ey;
-  for (int l = threadIdx.x; l < g.tn; l += blockDim.x) {
-    const int s = t * g.tn + l;
-    const uint32_t w = __ldg(flags + s);
+#pragma unroll 1
+  for (int l = threadIdx.x; l < TN; l += BT) {
+    const uint32_t w = __ldg(flags + (size_t)t * TN + l);
     const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live);
+    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
     if (!live) {
-      if (zfill) zero_fill(P, s);
+      if (zfill) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+      }
       continue;
     }
+    const uint32_t miss = ~w & kMaskBits;
     const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
-    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, local offset)
     const int cxm = lx == 0 ? -1 : 0, lxm = lx == 0 ? g.ex - 1 : lx - 1;
     const int cxp = lx == g.ex - 1 ? 1 : 0, lxp = lx == g.ex - 1 ? 0 : lx + 1;
     const int cym = ly == 0 ? -3 : 0, lym = (ly == 0 ? g.ey - 1 : ly - 1) * g.ex;
@@ -507,20 +545,42 @@ __global__ void __launch_bounds__(256) k_step_tile(const Planes<T> P, const uint
     const int czm = lz == 0 ? -9 : 0, lzm = (lz == 0 ? g.ez - 1 : lz - 1) * exy;
     const int czp = lz == g.ez - 1 ? 9 : 0, lzp = (lz == g.ez - 1 ? 0 : lz + 1) * exy;
     const int ly0 = ly * g.ex, lz0 = lz * exy;
-    T f[Q];
-    f[0] = __ldg(P.pre[0] + s);
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
+    auto up = [&](int i) {
       const int code = 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) +
                        (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
                        (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
       const int loc = (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx)) +
                       (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
                       (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
-      f[i] = __ldg(P.pre[i] + (snbr[code] * g.tn + loc));
+      return srel[code] + i * TN + loc;
+    };
+    T f[Q];
+    f[0] = __ldg(tb + l);
+    if (MODE == 0) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + up(i));
+      if (miss) {
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+          if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
+      }
+    } else {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : up(i)));
     }
-    bounce_back_fixup(f, w, P, s);
-    bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
+    const uint32_t ty = flag_type(w);
+    if (ty == VELOCITY_BC) {
+      const uint32_t b = flag_bc(w);
+      zou_he_velocity19<T>(f, flag_orient(w), bcv[3 * b], bcv[3 * b + 1], bcv[3 * b + 2]);
+    } else if (ty == PRESSURE_BC) {
+      zou_he_pressure19<T>(f, flag_orient(w), bcr[flag_bc(w)]);
+    }
+    T rho, vx, vy, vz;
+    moments19(f, rho, vx, vy, vz);
+    collide19(f, rho, vx, vy, vz, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
   }
 }
 
@@ -545,6 +605,7 @@ struct lbm_handle {
   double* bcr64 = nullptr;
   int nb = 0;
   int parity = 0;
+  int variant = 0;  // step-kernel variant (LBM_STEP_VARIANT), see launch_step
   bool geometry = false, initialized = false;
   long long step_count = 0, visited_total = 0, launches = 0;
   long long device_bytes = 0;
@@ -618,6 +679,19 @@ bool is_tiled(int layout) { return layout == LBM_LAYOUT_TILE || layout == LBM_LA
 
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g.nz); }
 
+template <typename T, int TN>
+void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
+  const unsigned nt = (unsigned)h->n_tiles;
+  const T* bv = (const T*)h->bcv;
+  const T* br = (const T*)h->bcr;
+  if (var == 1)
+    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, (T)h->d.omega);
+  else
+    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, (T)h->d.omega);
+}
+
 template <typename T>
 int launch_step(lbm_handle* h, const void* pre, void* post) {
   const Geo& g = h->g;
@@ -627,15 +701,32 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
     P.pre[i] = (const T*)pre + (size_t)i * g.ps;
     P.post[i] = (T*)post + (size_t)i * g.ps;
   }
+  // variants (LBM_STEP_VARIANT): 0 speculative + fix-up, 1 warp-uniform
+  // fast path else per-link select; 2 / 3 the same with a looser register cap
+  const int var = h->variant;
+  constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
+  const T* bv = (const T*)h->bcv;
+  const T* br = (const T*)h->bcr;
   if (!g.tiled) {
     const int bx = 128;
     dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
-    k_step_dense<T><<<grid, bx, 0, h->stream>>>(P, h->flags, (const T*)h->bcv, (const T*)h->bcr, g, om);
+    if (var == 1)
+      k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+    else if (var == 2)
+      k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+    else if (var == 3)
+      k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+    else
+      k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
   } else {
     if (h->n_tiles == 0) return 0;
-    const int bt = g.tn < 256 ? g.tn : 256;
-    k_step_tile<T><<<(unsigned)h->n_tiles, bt, 0, h->stream>>>(P, h->flags, h->nbr27, (const T*)h->bcv,
-                                                                (const T*)h->bcr, g, om);
+    switch (g.tn) {
+      case 32: launch_tiles<T, 32>(h, (const T*)pre, (T*)post, var); break;
+      case 64: launch_tiles<T, 64>(h, (const T*)pre, (T*)post, var); break;
+      case 128: launch_tiles<T, 128>(h, (const T*)pre, (T*)post, var); break;
+      case 256: launch_tiles<T, 256>(h, (const T*)pre, (T*)post, var); break;
+      default: launch_tiles<T, 512>(h, (const T*)pre, (T*)post, var); break;
+    }
   }
   h->launches += 1;
   return 0;
@@ -672,8 +763,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
       const int e = d.tile[a];
       if (e < 1 || (e & (e - 1))) return fail(LBM_EINVAL, "tile edges must be powers of two, got %d", e);
     }
-    if (d.tile[0] * d.tile[1] * d.tile[2] > 4096 || d.tile[0] * d.tile[1] * d.tile[2] < 32)
-      return fail(LBM_EINVAL, "tile must hold 32..4096 nodes");
+    if (d.tile[0] * d.tile[1] * d.tile[2] > 512 || d.tile[0] * d.tile[1] * d.tile[2] < 32)
+      return fail(LBM_EINVAL, "tile must hold 32..512 nodes");
     const int n3[3] = {d.nx, d.ny, d.nz};
     for (int a = 0; a < 3; ++a)
       if (d.periodic[a] && n3[a] % d.tile[a])
@@ -696,6 +787,12 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
   g.py = d.periodic[1] != 0;
   g.pzw = (d.periodic[2] != 0) && (nzg == d.nz);
   g.tiled = is_tiled(d.layout);
+  {
+    const char* zf = getenv("LBM_ZERO_FILL");  // A/B switch for the sector-completion stores
+    g.zero_fill = (zf && zf[0] == '0') ? 0 : 1;
+    const char* sv = getenv("LBM_STEP_VARIANT");
+    h->variant = sv ? atoi(sv) : 0;
+  }
   h->n_nodes = (long long)d.nx * d.ny * d.nz;
   if (!g.tiled) {
     g.nxp = (d.nx + 31) / 32 * 32;
@@ -714,6 +811,7 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     g.gy = (d.ny + g.ey - 1) / g.ey;
     g.gz = (d.nz + g.ez - 1) / g.ez;
     g.tn = g.ex * g.ey * g.ez;
+    g.ltn = ilog2(g.tn);
     g.nxp = d.nx;
     h->ntiles_grid = (long long)g.gx * g.gy * g.gz;
   }
@@ -848,7 +946,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         CKL();
       }
       h->n_slots = T * g.tn;
-      g.ps = (h->n_slots + 63) / 64 * 64;
+      g.ps = h->n_slots;  // AoSoA: 19 * ps elements = T tiles x 19 blocks
       h->nflags = h->n_slots;
       if ((rc = dev_alloc(h, &h->flags, (h->nflags > 0 ? h->nflags : 1) * 4))) goto done;
       if (h->nflags > 0) {

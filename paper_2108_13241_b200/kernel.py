@@ -174,12 +174,25 @@ class DeviceField:
     def allocated_tiles(self):
         return int(self._sim._handle.stats().n_tiles)
 
+    def _tiled(self):
+        return self.layout in (LayoutKind.TILE, LayoutKind.POINTER_TILE)
+
     def _get(self, which):
+        """(19, n_slots) host view of buffer `which`.  Tile layouts are stored
+        AoSoA (tile, direction, node) on the device; the view is transposed
+        to the reference's (direction, slot) indexing and written back by
+        flush()."""
         if which not in self._mirror:
-            arr = np.empty((Q, self.plane_stride), dtype=self.dtype)
+            raw = np.empty(Q * self.plane_stride, dtype=self.dtype)
             _lib.check(self._sim._handle.lib.lbm_get_field(self._sim._handle.h, which,
-                                                           _lib.ptr(arr)))
-            self._mirror[which] = arr
+                                                           _lib.ptr(raw)))
+            if self._tiled():
+                tn = int(np.prod(self._sim.tile))
+                T = self.plane_stride // tn
+                view = np.ascontiguousarray(raw.reshape(T, Q, tn).transpose(1, 0, 2)).reshape(Q, T * tn)
+            else:
+                view = raw.reshape(Q, self.plane_stride)
+            self._mirror[which] = view
         return self._mirror[which]
 
     @property
@@ -204,8 +217,14 @@ class DeviceField:
         if not self._mirror:
             return
         h = self._sim._handle
-        for which, arr in self._mirror.items():
-            _lib.check(h.lib.lbm_set_field(h.h, which, _lib.ptr(arr)))
+        for which, view in self._mirror.items():
+            if self._tiled():
+                tn = int(np.prod(self._sim.tile))
+                T = view.shape[1] // tn
+                raw = np.ascontiguousarray(view.reshape(Q, T, tn).transpose(1, 0, 2))
+            else:
+                raw = np.ascontiguousarray(view)
+            _lib.check(h.lib.lbm_set_field(h.h, which, _lib.ptr(raw)))
         self._mirror = {}
 
     def invalidate(self):
