@@ -1,0 +1,99 @@
+"""Multi-GPU leg of bench.py (launched by torchrun, one rank per GPU).
+
+Weak scaling of config C2: every rank owns a 512^3 z-slab of a z-periodic
+channel of global extent 512 x 512 x (512 N); ranks form a ring.  The step
+kernel stores the outgoing c_z = +-1 populations of its two boundary planes
+straight into the neighbours' ghost planes (CUDA IPC peer memory over
+NVLink), device flags order the steps.  Timing: barrier + synchronize, K
+steps timed with CUDA events on each rank's solver stream, MAX over ranks.
+"""
+
+import json
+import os
+import time
+
+import numpy as np
+
+
+def run_multi(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2108_13241_b200 as lb
+    from bench import BYTES_PER_NODE_F32, METRIC, ClockSampler, measured_peak
+    from paper_2108_13241_b200.distributed import channel_slab, connect_distributed, duct_slab
+
+    if os.environ.get("LBM_BENCH_SAME_GPU") == "1":
+        # functional check of the multi-rank path on a single-GPU box: every
+        # rank on device 0, gloo plumbing (NCCL refuses two ranks per GPU)
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        dev = "cpu"
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = "cuda"
+    workload = args.workload or "channel512"
+    if workload == "duct":
+        geom, spec = duct_slab(1024, 1024, 256, rank, world)
+        params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
+        desc = (f"C5: D3Q19 duct 1024x1024x{256 * world} along z, z-slabs of 1024x1024x256 per "
+                "GPU, velocity inlet / pressure outlet, fp32")
+        periodic = False
+    else:
+        geom, spec = channel_slab(512, 512, 512, rank, world)
+        params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25)
+        desc = (f"C2 weak scaling: D3Q19 channel 512x512x{512 * world} (z-periodic ring), "
+                "z-slab of 512^3 per GPU, fp32")
+        periodic = True
+    sim = lb.Simulation(geom, params, layout="dense", scalar=np.float32, device=local, slab=spec)
+    connect_distributed(sim, periodic_z=periodic)
+    sim.initialize(1.0)
+    sim.step(args.warmup)
+    launches0 = sim.launches_total
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        sim.step(args.steps)
+        t1 = time.perf_counter()
+    dist.barrier()
+    ms = sim.last_step_ms
+    t = torch.tensor([ms, t1 - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, wall_max = float(t[0]), float(t[1])
+    nons = torch.tensor([sim.active_node_count], dtype=torch.float64, device=dev)
+    dist.all_reduce(nons)
+    total_nons = float(nons[0])
+    launches = sim.launches_total - launches0
+    clocks = clk.summary()
+    mlups = total_nons * args.steps / (ms_max / 1e3) / 1e6
+    peak, peak_src = measured_peak()
+    per_gpu_nodes = total_nons / world
+    achieved = per_gpu_nodes * BYTES_PER_NODE_F32 / (ms_max / args.steps / 1e3) / 1e9
+    finite = True
+    try:
+        sim.check_finite()
+    except Exception:
+        finite = False
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": desc, "layout": "dense", "nodes_per_gpu": int(per_gpu_nodes),
+                       "l2": "state per GPU >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"z-slab x{world}, fused peer-store halo (CUDA IPC)"},
+            "mlups_per_gpu": mlups / world,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "bytes_per_node": BYTES_PER_NODE_F32},
+            "e2e": None, "gpu_launches": int(launches), "clocks": clocks,
+            "wall_s_max": wall_max, "finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+    sim.close()
+    dist.barrier()
+    dist.destroy_process_group()

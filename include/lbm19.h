@@ -119,6 +119,10 @@ int lbm_init_equilibrium(lbm_t* h, const double* rho, const double* ux,
                          double ux0, double uy0, double uz0);
 
 int lbm_step(lbm_t* h, int64_t n);
+/* Enqueue n steps without waiting (several slabs driven from one thread);
+ * lbm_synchronize waits and records the device time of the batch. */
+int lbm_step_async(lbm_t* h, int64_t n);
+int lbm_synchronize(lbm_t* h);
 int lbm_set_omega(lbm_t* h, double omega);
 
 /* f64 (nz, ny, nx) arrays; solid nodes report 0. Any pointer may be NULL. */
@@ -144,6 +148,20 @@ int lbm_get_flags(lbm_t* h, uint32_t* out);
 /* tiles (T, 3) as (tx, ty, tz), nbr27 (T, 27); either may be NULL to query T. */
 int lbm_get_tile_index(lbm_t* h, int32_t* tiles, int32_t* nbr27, int64_t* n_tiles);
 int lbm_get_stats(lbm_t* h, lbm_stats* out);
+
+/* z-slab halo exchange (multi-GPU, dense layouts).  Each slab handle covers
+ * global planes [z0, z0 + nz); after every step the outgoing populations of
+ * its two boundary planes are stored by the step kernel itself straight into
+ * the neighbouring slab's ghost plane (peer memory: same process = device
+ * pointers + peer access, other process = CUDA IPC), and device-side flags
+ * order the steps (no host round trip).  lbm_halo_export writes an opaque
+ * LBM_HALO_BLOB_BYTES blob the caller ships to the neighbours (e.g. with
+ * torch.distributed.all_gather_object); lbm_halo_connect opens the lower and
+ * upper neighbour's blob (NULL = no neighbour on that side).  All slabs must
+ * then make the same sequence of init / step calls. */
+#define LBM_HALO_BLOB_BYTES 512
+int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes);
+int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob);
 
 /* scalar per-node math (host), same source as the device kernel.
  * dtype LBM_F32 computes in float32 (values round-tripped through double). */

@@ -17,6 +17,7 @@ LBM_OK, LBM_EINVAL, LBM_ESTATE, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EDIVERGED 
     0, -1, -2, -3, -4, -5, -6
 LBM_F32, LBM_F64 = 0, 1
 LAYOUT_CODES = {"dense": 0, "tile": 1, "bitmask_node": 2, "pointer_tile": 3}
+HALO_BLOB_BYTES = 512
 
 
 class LbmDesc(C.Structure):
@@ -53,6 +54,8 @@ SIGNATURES = [
     ("lbm_set_geometry", C.c_int, [P, P, P, P, P, P, P, P, P, I32]),
     ("lbm_init_equilibrium", C.c_int, [P, P, P, P, P, D, D, D, D]),
     ("lbm_step", C.c_int, [P, I64]),
+    ("lbm_step_async", C.c_int, [P, I64]),
+    ("lbm_synchronize", C.c_int, [P]),
     ("lbm_set_omega", C.c_int, [P, D]),
     ("lbm_get_macroscopic", C.c_int, [P, P, P, P, P]),
     ("lbm_check_finite", C.c_int, [P, C.POINTER(I32), P]),
@@ -65,6 +68,8 @@ SIGNATURES = [
     ("lbm_get_flags", C.c_int, [P, P]),
     ("lbm_get_tile_index", C.c_int, [P, P, P, C.POINTER(I64)]),
     ("lbm_get_stats", C.c_int, [P, C.POINTER(LbmStats)]),
+    ("lbm_halo_export", C.c_int, [P, P, C.POINTER(C.c_size_t)]),
+    ("lbm_halo_connect", C.c_int, [P, P, P]),
     ("lbm19_feq", C.c_int, [I32, D, PD, PD]),
     ("lbm19_moments", C.c_int, [I32, PD, PD, PD]),
     ("lbm19_collide", C.c_int, [I32, PD, D, PD]),

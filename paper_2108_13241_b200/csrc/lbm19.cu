@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
 #include <string>
 #include <vector>
 
@@ -400,6 +401,56 @@ __device__ __forceinline__ bool sector_needs_zero(bool nonsolid) {
   return (act & grp) != 0u;
 }
 
+// z-slab halo, fused into the step: the outgoing populations of the two
+// boundary planes (c_z = -1 from z = 0, c_z = +1 from z = nz - 1) are stored
+// straight into the neighbouring slab's ghost plane (peer memory over
+// NVLink / IPC), next to the node-local store.  Null pointers: no neighbour.
+__host__ __device__ constexpr int kZm(int j) { return 10 + 2 * j; }  // c_z = -1: 10 12 14 16 18
+__host__ __device__ constexpr int kZp(int j) { return 9 + 2 * j; }   // c_z = +1: 9 11 13 15 17
+template <typename T>
+struct Halo {
+  T* lo[5];  // lower neighbour's upper ghost plane, directions kZm
+  T* hi[5];  // upper neighbour's lower ghost plane, directions kZp
+};
+
+__global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int need_hi,
+                            unsigned long long target, int* err) {
+  const long long t0 = clock64();
+  const volatile unsigned long long* vs = sync;
+  while ((need_lo && vs[0] < target) || (need_hi && vs[1] < target)) {
+    __nanosleep(200);
+    if (clock64() - t0 > 60LL * 2000000000LL) {  // ~1 min at 2 GHz: a neighbour is gone
+      atomicOr(err, 1);
+      return;
+    }
+  }
+  __threadfence_system();
+}
+
+__global__ void k_halo_signal(unsigned long long* lo_slot, unsigned long long* hi_slot,
+                              unsigned long long value) {
+  __threadfence_system();
+  if (lo_slot) *(volatile unsigned long long*)lo_slot = value;
+  if (hi_slot) *(volatile unsigned long long*)hi_slot = value;
+  __threadfence_system();
+}
+
+// initial ghost fill (after initialize / set_pdf): boundary planes of `pre`
+template <typename T>
+__global__ void k_halo_push(const T* __restrict__ pre, Halo<T> H, Geo g) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (x >= g.nxp) return;
+  const int row = y * g.nxp + x;
+  const int s0 = (int)g.plane + row, s1 = g.nz * (int)g.plane + row;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (H.lo[0]) H.lo[j][row] = pre[(long long)kZm(j) * g.ps + s0];
+    if (H.hi[0]) H.hi[j][row] = pre[(long long)kZp(j) * g.ps + s1];
+  }
+  __threadfence_system();
+}
+
 // 19 direction planes of one buffer, resolved on the host once per launch, so
 // every access is a 32-bit slot offset from a per-direction base pointer
 template <typename T>
@@ -465,7 +516,8 @@ __device__ __forceinline__ void zero_fill(const Planes<T>& P, int s) {
 template <typename T, int MODE, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
                                                    const T* __restrict__ bcv,
-                                                   const T* __restrict__ bcr, Geo g, T om) {
+                                                   const T* __restrict__ bcr, Geo g, T om,
+                                                   const Halo<T> H) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
@@ -499,6 +551,18 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   f[0] = __ldg(P.pre[0] + s);
   gather<T, MODE>(f, miss, fast, P, s, up);
   bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
+  if ((z == 0 && H.lo[0]) || (z == g.nz - 1 && H.hi[0])) {
+    const int row = y * g.nxp + x;
+    if (z == 0 && H.lo[0]) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) H.lo[j][row] = f[kZm(j)];
+    }
+    if (z == g.nz - 1 && H.hi[0]) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) H.hi[j][row] = f[kZp(j)];
+    }
+    __threadfence_system();
+  }
 }
 
 // Sparse tiles, AoSoA storage f[tile][i][TN]: one CTA per kept tile.  All
@@ -614,6 +678,19 @@ struct lbm_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double* scratch = nullptr;   // reductions
   unsigned long long* uscratch = nullptr;
+  // z-slab halo (fused peer stores); see k_step_dense and lbm_halo_connect
+  struct Peer {
+    bool on = false, ipc = false;
+    void* f[2] = {nullptr, nullptr};
+    unsigned long long* sync = nullptr;
+    long long ps = 0;
+    int nz = 0;
+  } lo, hi;
+  unsigned long long* sync = nullptr;  // [0] written by the lower, [1] by the upper neighbour
+  int* herr = nullptr;
+  unsigned long long epoch = 0;        // halo pushes done by this handle
+  bool halo_dirty = true;
+  bool pending = false;                // lbm_step_async issued, not yet synchronised
 };
 
 namespace {
@@ -679,6 +756,37 @@ bool is_tiled(int layout) { return layout == LBM_LAYOUT_TILE || layout == LBM_LA
 
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g.nz); }
 
+// peer ghost planes of buffer q (lockstep: every slab is at the same parity)
+template <typename T>
+Halo<T> make_halo(const lbm_handle* h, int q) {
+  Halo<T> H;
+  for (int j = 0; j < 5; ++j) {
+    H.lo[j] = h->lo.on ? (T*)h->lo.f[q] + (size_t)kZm(j) * h->lo.ps + (size_t)(h->lo.nz + 1) * h->g.plane
+                       : nullptr;
+    H.hi[j] = h->hi.on ? (T*)h->hi.f[q] + (size_t)kZp(j) * h->hi.ps : nullptr;
+  }
+  return H;
+}
+
+bool halo_on(const lbm_handle* h) { return h->lo.on || h->hi.on; }
+
+void halo_signal(lbm_handle* h) {
+  h->epoch += 1;
+  k_halo_signal<<<1, 1, 0, h->stream>>>(h->lo.on ? h->lo.sync + 1 : nullptr,
+                                         h->hi.on ? h->hi.sync + 0 : nullptr, h->epoch);
+}
+
+void halo_wait(lbm_handle* h) {
+  k_halo_wait<<<1, 1, 0, h->stream>>>(h->sync, h->lo.on, h->hi.on, h->epoch, h->herr);
+}
+
+template <typename T>
+void halo_push(lbm_handle* h) {
+  const Halo<T> H = make_halo<T>(h, h->parity);
+  dim3 grid((h->g.nxp + 127) / 128, h->g.ny);
+  k_halo_push<T><<<grid, 128, 0, h->stream>>>((const T*)h->f[h->parity], H, h->g);
+}
+
 template <typename T, int TN>
 void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   constexpr int BT = TN < 256 ? TN : 256;
@@ -710,14 +818,15 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
   if (!g.tiled) {
     const int bx = 128;
     dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
+    const Halo<T> H = make_halo<T>(h, 1 - h->parity);
     if (var == 1)
-      k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+      k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
     else if (var == 2)
-      k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+      k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
     else if (var == 3)
-      k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+      k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
     else
-      k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om);
+      k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
   } else {
     if (h->n_tiles == 0) return 0;
     switch (g.tn) {
@@ -820,6 +929,10 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
   if (e == cudaSuccess) e = cudaMalloc(&h->scratch, 4096 * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&h->uscratch, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&h->sync, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(h->sync, 0, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&h->herr, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(h->herr, 0, sizeof(int));
   if (e != cudaSuccess) {
     lbm_destroy(h);
     return fail(LBM_ECUDA, "stream/event setup: %s", cudaGetErrorString(e));
@@ -832,9 +945,19 @@ void lbm_destroy(lbm_t* h) {
   if (!h) return;
   DeviceGuard dg(h->d.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
+  for (lbm_handle::Peer* pr : {&h->lo, &h->hi}) {
+    if (pr->on && pr->ipc) {
+      cudaIpcCloseMemHandle(pr->f[0]);
+      cudaIpcCloseMemHandle(pr->f[1]);
+      cudaIpcCloseMemHandle(pr->sync);
+    }
+    pr->on = false;
+  }
   free_geometry(h);
   dev_free(h->scratch);
   dev_free(h->uscratch);
+  dev_free(h->sync);
+  dev_free(h->herr);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -1039,6 +1162,7 @@ int lbm_init_equilibrium(lbm_t* h, const double* rho, const double* ux, const do
   for (int k = 0; k < 4; ++k) dev_free(dev[k]);
   if (rc) return rc;
   h->initialized = true;
+  h->halo_dirty = true;
   h->step_count = h->visited_total = 0;
   return 0;
 }
@@ -1050,33 +1174,62 @@ int lbm_set_omega(lbm_t* h, double omega) {
   return 0;
 }
 
-int lbm_step(lbm_t* h, int64_t n) {
+int lbm_step_async(lbm_t* h, int64_t n) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (n < 0) return fail(LBM_EINVAL, "n_steps must be >= 0, got %lld", (long long)n);
   if (!h->initialized) return fail(LBM_ESTATE, "initialize() must run before stepping");
   DeviceGuard dg(h->d.device);
+  const bool halo = halo_on(h);
+  if (halo && h->halo_dirty && n > 0) {
+    // ghost planes of `pre` after initialize / set_pdf: push, then signal
+    if (h->esize == 4) halo_push<float>(h); else halo_push<double>(h);
+    halo_signal(h);
+    h->halo_dirty = false;
+  }
   CK(cudaEventRecord(h->ev0, h->stream));
   for (int64_t k = 0; k < n; ++k) {
     const void* pre = h->f[h->parity];
     void* post = h->f[1 - h->parity];
+    if (halo) halo_wait(h);   // neighbours pushed my ghosts and finished reading theirs
     if (h->esize == 4)
       launch_step<float>(h, pre, post);
     else
       launch_step<double>(h, pre, post);
+    if (halo) halo_signal(h);
     h->parity ^= 1;
   }
   CKL();
   CK(cudaEventRecord(h->ev1, h->stream));
-  CK(cudaEventSynchronize(h->ev1));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
-  h->last_ms = ms;
+  h->pending = true;
   h->step_count += n;
   const long long visits = (h->d.layout == LBM_LAYOUT_DENSE) ? h->n_nodes
                            : (h->d.layout == LBM_LAYOUT_BITMASK_NODE) ? h->n_nonsolid
                                                                        : h->n_slots;
   h->visited_total += n * visits;
   return 0;
+}
+
+int lbm_synchronize(lbm_t* h) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  DeviceGuard dg(h->d.device);
+  if (!h->pending) return 0;
+  h->pending = false;
+  CK(cudaEventSynchronize(h->ev1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+  h->last_ms = ms;
+  if (halo_on(h)) {
+    int herr = 0;
+    CK(cudaMemcpy(&herr, h->herr, 4, cudaMemcpyDeviceToHost));
+    if (herr) return fail(LBM_ENCCL, "halo wait timed out: a neighbouring slab stopped stepping");
+  }
+  return 0;
+}
+
+int lbm_step(lbm_t* h, int64_t n) {
+  int rc = lbm_step_async(h, n);
+  if (rc) return rc;
+  return lbm_synchronize(h);
 }
 
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
@@ -1202,7 +1355,10 @@ static int pdf_io(lbm_t* h, int which, void* host, bool get) {
 }
 
 int lbm_get_pdf(lbm_t* h, int32_t which, void* out) { return pdf_io(h, which, out, true); }
-int lbm_set_pdf(lbm_t* h, int32_t which, const void* in) { return pdf_io(h, which, (void*)in, false); }
+int lbm_set_pdf(lbm_t* h, int32_t which, const void* in) {
+  if (h) h->halo_dirty = true;
+  return pdf_io(h, which, (void*)in, false);
+}
 
 static int field_io(lbm_t* h, int which, void* host, bool get) {
   if (!h || !host) return fail(LBM_EINVAL, "NULL argument");
@@ -1219,7 +1375,10 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
 }
 
 int lbm_get_field(lbm_t* h, int32_t which, void* out) { return field_io(h, which, out, true); }
-int lbm_set_field(lbm_t* h, int32_t which, const void* in) { return field_io(h, which, (void*)in, false); }
+int lbm_set_field(lbm_t* h, int32_t which, const void* in) {
+  if (h) h->halo_dirty = true;
+  return field_io(h, which, (void*)in, false);
+}
 
 int lbm_get_slot_of(lbm_t* h, int32_t* out) {
   if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
@@ -1282,6 +1441,102 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->last_step_ms = h->last_ms;
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
+  return 0;
+}
+
+// ------------------------------------------------------------- halo C-ABI
+namespace {
+struct HaloBlob {
+  uint32_t magic;
+  int32_t device, esize, nz, ny, nxp;
+  int64_t pid, ps;
+  void* f[2];
+  void* sync;
+  cudaIpcMemHandle_t ipc_f[2];
+  cudaIpcMemHandle_t ipc_sync;
+};
+constexpr uint32_t kHaloMagic = 0x4C424D48u;  // "LBMH"
+static_assert(sizeof(HaloBlob) <= LBM_HALO_BLOB_BYTES, "halo blob too large");
+
+int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
+  if (b.magic != kHaloMagic) return fail(LBM_EINVAL, "not a halo blob");
+  if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp)
+    return fail(LBM_EINVAL, "neighbouring slab has a different dtype or x/y extent");
+  if (b.pid == (int64_t)getpid()) {
+    if (b.device != h->d.device) {
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, h->d.device, b.device));
+      if (!can) return fail(LBM_ENCCL, "device %d cannot access peer %d", h->d.device, b.device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(LBM_ENCCL, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    pr.f[0] = b.f[0];
+    pr.f[1] = b.f[1];
+    pr.sync = (unsigned long long*)b.sync;
+    pr.ipc = false;
+  } else {
+    CK(cudaIpcOpenMemHandle(&pr.f[0], b.ipc_f[0], cudaIpcMemLazyEnablePeerAccess));
+    CK(cudaIpcOpenMemHandle(&pr.f[1], b.ipc_f[1], cudaIpcMemLazyEnablePeerAccess));
+    void* sy = nullptr;
+    CK(cudaIpcOpenMemHandle(&sy, b.ipc_sync, cudaIpcMemLazyEnablePeerAccess));
+    pr.sync = (unsigned long long*)sy;
+    pr.ipc = true;
+  }
+  pr.ps = b.ps;
+  pr.nz = b.nz;
+  pr.on = true;
+  return 0;
+}
+}  // namespace
+
+int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
+  if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_export");
+  if (h->g.tiled) return fail(LBM_EINVAL, "z-slab halos need a dense layout");
+  DeviceGuard dg(h->d.device);
+  HaloBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kHaloMagic;
+  b.device = h->d.device;
+  b.esize = h->esize;
+  b.nz = h->g.nz;
+  b.ny = h->g.ny;
+  b.nxp = h->g.nxp;
+  b.pid = (int64_t)getpid();
+  b.ps = h->g.ps;
+  b.f[0] = h->f[0];
+  b.f[1] = h->f[1];
+  b.sync = h->sync;
+  CK(cudaIpcGetMemHandle(&b.ipc_f[0], h->f[0]));
+  CK(cudaIpcGetMemHandle(&b.ipc_f[1], h->f[1]));
+  CK(cudaIpcGetMemHandle(&b.ipc_sync, h->sync));
+  memset(blob, 0, LBM_HALO_BLOB_BYTES);
+  memcpy(blob, &b, sizeof(b));
+  if (bytes) *bytes = LBM_HALO_BLOB_BYTES;
+  return 0;
+}
+
+int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_connect");
+  if (h->g.tiled) return fail(LBM_EINVAL, "z-slab halos need a dense layout");
+  if (h->g.pzw && (lo_blob || hi_blob))
+    return fail(LBM_EINVAL, "a whole-domain periodic handle wraps z itself; it takes no halo");
+  DeviceGuard dg(h->d.device);
+  CK(cudaStreamSynchronize(h->stream));
+  int rc = 0;
+  HaloBlob b;
+  if (lo_blob) {
+    memcpy(&b, lo_blob, sizeof(b));
+    if ((rc = open_peer(h, b, h->lo))) return rc;
+  }
+  if (hi_blob) {
+    memcpy(&b, hi_blob, sizeof(b));
+    if ((rc = open_peer(h, b, h->hi))) return rc;
+  }
+  h->halo_dirty = true;
   return 0;
 }
 

@@ -256,7 +256,7 @@ class Simulation:
     (reference kernel.py:155-311)."""
 
     def __init__(self, geometry, params, layout=LayoutKind.DENSE, scalar=np.float64,
-                 device=0, tile=(8, 8, 8)):
+                 device=0, tile=(8, 8, 8), slab=None):
         self.geometry = geometry
         self.params = params
         self.layout = LayoutKind.parse(layout)
@@ -266,9 +266,12 @@ class Simulation:
         self.device = int(device)
         self.tile = tuple(int(t) for t in tile)
         desc = geometry.descriptors
+        self.slab = slab
+        nzg, z0, glo, ghi = (None, 0, None, None) if slab is None else \
+            (slab.nz_global, slab.z0, slab.ghost_lo, slab.ghost_hi)
         self._handle = _Handle(_desc(desc.dims, desc.periodic, self.dtype, self.layout,
-                                     self.tile, self.device, params.omega))
-        _upload_geometry(self._handle, desc, geometry.boundary_values)
+                                     self.tile, self.device, params.omega, nz_global=nzg, z0=z0))
+        _upload_geometry(self._handle, desc, geometry.boundary_values, ghost_lo=glo, ghost_hi=ghi)
         self.field = DeviceField(self)
         self.initialized = False
 
@@ -330,14 +333,21 @@ class Simulation:
         self.field.frozen = True
 
     # -- stepping ---------------------------------------------------------
-    def step(self, n=1):
+    def step(self, n=1, block=True):
         """Advance n time steps on the device (reference kernel.py:239-252,
-        n = 1).  Returns after the device finished."""
+        n = 1).  Returns after the device finished unless block=False (then
+        call synchronize(); used to drive several slabs from one thread)."""
         if not self.initialized:
             raise RuntimeError("initialize() must run before stepping")
         self.field.flush()
         h = self._handle
-        _lib.check(h.lib.lbm_step(h.h, int(n)), "step")
+        if block:
+            _lib.check(h.lib.lbm_step(h.h, int(n)), "step")
+        else:
+            _lib.check(h.lib.lbm_step_async(h.h, int(n)), "step")
+
+    def synchronize(self):
+        _lib.check(self._handle.lib.lbm_synchronize(self._handle.h), "synchronize")
 
     def run(self, n_steps, observers=(), check_divergence_every=None):
         """Advance n_steps, firing each (every_k, callback) observer at steps
@@ -423,6 +433,21 @@ class Simulation:
             raise ValueError(f"state must have shape {(Q, nz, ny, nx)}, got {f.shape}")
         _lib.check(self._handle.lib.lbm_set_pdf(self._handle.h, 0 if which == "pre" else 1,
                                                 _lib.ptr(f)))
+
+    # -- z-slab halo ---------------------------------------------------------
+    def halo_blob(self):
+        """Opaque bytes describing this slab's PDF buffers for its neighbours
+        (CUDA IPC handles + device pointers), see lbm_halo_export."""
+        buf = (C.c_char * _lib.HALO_BLOB_BYTES)()
+        n = C.c_size_t(0)
+        _lib.check(self._handle.lib.lbm_halo_export(self._handle.h, buf, C.byref(n)))
+        return bytes(buf)[:n.value]
+
+    def connect_halo(self, lo_blob=None, hi_blob=None):
+        """Attach the lower / upper neighbour slab (None: no neighbour)."""
+        lo = None if lo_blob is None else C.create_string_buffer(lo_blob, len(lo_blob))
+        hi = None if hi_blob is None else C.create_string_buffer(hi_blob, len(hi_blob))
+        _lib.check(self._handle.lib.lbm_halo_connect(self._handle.h, lo, hi), "halo connect")
 
     def flag_words(self):
         nx, ny, nz = self.geometry.dims
