@@ -65,6 +65,18 @@ def build_workload(name, rank=0, world=1):
         desc = ("C2: D3Q19 dense channel 512^3, velocity inlet u=0.05 (x=0), pressure "
                 "outlet rho=1 (x=511), bounce-back y walls, periodic z, nu=0.25, fp32")
         return geom, params, "dense", desc, 1.0
+    if name == "cavity64":
+        geom = lb.build_cavity(64, 64, 64, 0.1)
+        params = lb.FlowParams.from_reynolds(U=0.1, L=63, Re=100)
+        desc = "C1: D3Q19 lid-driven cavity 64^3, Re 100, fp32 (L2-resident; parity config)"
+        return geom, params, "dense", desc, 1.0
+    if name.startswith("porous512@"):
+        phi = float(name.split("@")[1])
+        geom = lb.build_porous_random(512, phi, seed=0, radius_range=(4, 32))
+        params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
+        desc = (f"C3: D3Q19 random-sphere porous medium 512^3, phi target {phi} "
+                f"(achieved {geom.porosity:.3f}), pointer-tile 8^3, fp32")
+        return geom, params, "pointer_tile", desc, 1.008
     if name == "porous512":
         geom = lb.build_porous_random(512, 0.5, seed=0, radius_range=(4, 32))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
