@@ -258,7 +258,13 @@ def main():
     geom, params, layout, desc, rho0 = build_workload(workload)
     if args.variants:
         for v in args.variants.split(","):
-            os.environ["LBM_STEP_VARIANT"] = v
+            # "3" selects LBM_STEP_VARIANT=3; "KEY=VAL;KEY=VAL" sets library switches
+            if "=" in v:
+                for kv in v.split(";"):
+                    k, val = kv.split("=")
+                    os.environ[k] = val
+            else:
+                os.environ["LBM_STEP_VARIANT"] = v
             sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
             sim.initialize(rho0)
             sim.step(args.warmup)

@@ -260,6 +260,16 @@ __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
 }
 
+// live-brick masks: bit b of tile t is set iff brick b holds a non-solid node
+__global__ void k_brick_mask(uint32_t* __restrict__ bmask, const uint32_t* __restrict__ flags, Geo g,
+                             long long nslots) {
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslots || flag_type(flags[s]) == SOLID) return;
+  const long long t = s >> g.ltn;
+  const int b = (int)(s & (g.tn - 1)) >> (g.lbx + g.lby + g.lbz);
+  atomicOr(bmask + 4 * t + (b >> 5), 1u << (b & 31));
+}
+
 // ------------------------------------------------------------ init / readback
 template <typename T>
 __global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
@@ -603,7 +613,8 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
 template <typename T, int TN, int MODE, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-             const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om) {
+             const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+             const uint32_t* __restrict__ bmask) {
   constexpr int BT = TN < 256 ? TN : 256;
   __shared__ int srel[27];
   const int t = blockIdx.x;
@@ -611,16 +622,50 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
     const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
     srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);  // absent: masked links, own tile
   }
-  __syncthreads();
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
+  // MODE 2: threads cover only the tile's live bricks (sector-sized bricks
+  // holding >= 1 non-solid node, a 128-bit mask per tile), so a sparse tile
+  // costs lanes in proportion to its live sectors, not its 512 slots
+  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+  int pre_cnt[4] = {0, 0, 0, 0};
+  int work = TN;
+  bool dense_tile = true;
+  if (MODE == 2) {
+    int acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      m[q] = __ldg(bmask + 4LL * t + q);
+      pre_cnt[q] = acc;
+      acc += __popc(m[q]);
+    }
+    work = ((acc << lbn) + 31) & ~31;  // whole warps; lanes past acc*bn idle
+    dense_tile = acc == (TN >> lbn);   // every brick live: identity mapping
+  }
+  __syncthreads();
 #pragma unroll 1
-  for (int l = threadIdx.x; l < TN; l += BT) {
-    const uint32_t w = __ldg(flags + (size_t)t * TN + l);
+  for (int k = threadIdx.x; k < work; k += BT) {
+    int l = k;
+    bool in = true;
+    if (MODE == 2 && !dense_tile) {
+      const int j = k >> lbn;  // live-brick ordinal
+      in = j < pre_cnt[3] + __popc(m[3]);
+      int q = 3;
+      if (j < pre_cnt[3]) q = 2;
+      if (j < pre_cnt[2]) q = 1;
+      if (j < pre_cnt[1]) q = 0;
+      const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
+      const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
+      const uint32_t pos = __fns(mq, 0, j - pq + 1);
+      const int b = in ? q * 32 + (int)pos : 0;
+      l = (b << lbn) | (k & (bn - 1));
+    }
+    const uint32_t w = in ? __ldg(flags + (size_t)t * TN + l) : 0u;
     const bool live = flag_type(w) != SOLID;
     const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
     if (!live) {
-      if (zfill) {
+      if (zfill && in) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
       }
@@ -648,7 +693,7 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
     };
     T f[Q];
     f[0] = __ldg(tb + l);
-    if (MODE == 0) {
+    if (MODE != 1) {
 #pragma unroll
       for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + up(i));
       if (miss) {
@@ -690,6 +735,7 @@ struct lbm_handle {
   int* rank = nullptr;    // tile rank grid
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
+  uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
   void* bcv = nullptr;    // (nb, 3) storage type
   void* bcr = nullptr;    // (nb) storage type
   uint8_t* bckind64 = nullptr;
@@ -778,6 +824,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->rank);
   dev_free(h->tiles);
   dev_free(h->nbr27);
+  dev_free(h->bmask);
   dev_free(h->bcv);
   dev_free(h->bcr);
   dev_free(h->bckind64);
@@ -786,6 +833,7 @@ void free_geometry(lbm_handle* h) {
   h->f[0] = h->f[1] = nullptr;
   h->flags = nullptr;
   h->rank = h->tiles = h->nbr27 = nullptr;
+  h->bmask = nullptr;
   h->bcv = h->bcr = nullptr;
   h->bckind64 = nullptr;
   h->bcv64 = h->bcr64 = nullptr;
@@ -844,10 +892,13 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const unsigned nt = (unsigned)h->n_tiles;
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
+  const T om = (T)h->d.omega;
   if (var == 1)
-    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, (T)h->d.omega);
+    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+  else if (var == 2)
+    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
   else
-    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, (T)h->d.omega);
+    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
 }
 
 template <typename T>
@@ -1145,6 +1196,12 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       if (h->nflags > 0) {
         k_flags_tile<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(
             h->flags, h->tiles, dtype_, dorient, dbc, glo, ghi, g, h->nflags, nb, derr, h->uscratch);
+        CKL();
+      }
+      if ((rc = dev_alloc(h, &h->bmask, (T > 0 ? T : 1) * 16))) goto done;
+      CK(cudaMemsetAsync(h->bmask, 0, (T > 0 ? T : 1) * 16, h->stream));
+      if (h->nflags > 0) {
+        k_brick_mask<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(h->bmask, h->flags, g, h->nflags);
         CKL();
       }
       h->sm.rank = h->rank;
