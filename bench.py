@@ -33,7 +33,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MLUPS per GPU and whole box (1/2/4/8 B200) and % of HBM roofline vs CPU ref"
-BYTES_PER_NODE_F32 = 19 * 4 * 2 + 4
+BYTES_PER_NODE_F32 = 19 * 4 * 2 + 4     # with one flag word per node
+PDF_BYTES_PER_NODE_F32 = 19 * 4 * 2
 
 
 def measured_peak():
@@ -273,9 +274,11 @@ def main():
             nons = sim.active_node_count
             mlups = nons * args.steps / (ms / 1e3) / 1e6
             peak, _ = measured_peak()
-            frac = nons * BYTES_PER_NODE_F32 / (ms / args.steps / 1e3) / 1e9 / peak
+            alg = nons * PDF_BYTES_PER_NODE_F32 + int(sim.stats().meta_bytes_per_step)
+            frac = alg / (ms / args.steps / 1e3) / 1e9 / peak
             print(json.dumps({"workload": workload, "variant": v, "mlups": round(mlups),
-                              "frac": round(frac, 4), "ms_per_step": ms / args.steps}), flush=True)
+                              "frac": round(frac, 4), "alg_B_per_node": round(alg / nons, 2),
+                              "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
         return
     sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
@@ -292,9 +295,11 @@ def main():
     mlups = nons * args.steps / (ms / 1e3) / 1e6
     peak, peak_src = measured_peak()
     per_launch_ms = ms / launches
-    alg_bytes = nons * BYTES_PER_NODE_F32
-    if layout == "pointer_tile":
-        alg_bytes += int(st.n_tiles) * (27 * 4)
+    # algorithmic bytes per launch: 19 reads + 19 writes of fp32 per non-solid
+    # node, plus the flag / index bytes this design's step reads (dense: flag
+    # words of non-uniform warp chunks + the uniform-chunk bitmap; tiles:
+    # nbr27 + brick masks + flag words of live bricks)
+    alg_bytes = nons * PDF_BYTES_PER_NODE_F32 + int(st.meta_bytes_per_step)
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     sane = bool(np.isfinite(sim.total_mass()))
     sim.close()
@@ -339,8 +344,10 @@ def main():
                      "frac": achieved / peak, "traffic": ncu_traffic(workload),
                      "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes,
-                     "bytes_per_node": BYTES_PER_NODE_F32,
-                     "frac_152B": nons * 152 / (per_launch_ms / 1e3) / 1e9 / peak},
+                     "alg_bytes_per_node": alg_bytes / nons,
+                     "meta_bytes_per_launch": int(st.meta_bytes_per_step),
+                     "frac_152B": nons * 152 / (per_launch_ms / 1e3) / 1e9 / peak,
+                     "frac_156B": nons * 156 / (per_launch_ms / 1e3) / 1e9 / peak},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "finite": sane,
     }

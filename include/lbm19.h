@@ -89,6 +89,7 @@ typedef struct lbm_stats {
   int64_t device_bytes;     /* bytes allocated on the device */
   int64_t launches_total;   /* kernels launched by lbm_step so far */
   double last_step_ms;      /* device time of the last lbm_step call (CUDA events) */
+  int64_t meta_bytes_per_step; /* flag / index bytes the step kernel reads per step */
   int32_t parity;
   int32_t initialized;
 } lbm_stats;

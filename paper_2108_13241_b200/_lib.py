@@ -34,7 +34,8 @@ class LbmStats(C.Structure):
                 ("plane_stride", C.c_int64), ("n_tiles", C.c_int64),
                 ("step_count", C.c_int64), ("visited_nodes_total", C.c_int64),
                 ("device_bytes", C.c_int64), ("launches_total", C.c_int64),
-                ("last_step_ms", C.c_double), ("parity", C.c_int32),
+                ("last_step_ms", C.c_double), ("meta_bytes_per_step", C.c_int64),
+                ("parity", C.c_int32),
                 ("initialized", C.c_int32)]
 
 

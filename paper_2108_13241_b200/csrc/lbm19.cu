@@ -260,6 +260,19 @@ __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
 }
 
+// dense: bit c of the uniform-chunk bitmap is set iff the 32 nodes of warp
+// chunk c (flag index 32c .. 32c + 31) are all FLUID / BOUNCE_BACK_WALL with
+// a full neighbour mask -- such warps skip the per-node flag load
+__global__ void k_uniform_bits(uint32_t* __restrict__ ubits, const uint32_t* __restrict__ flags,
+                               long long nflags) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t w = k < nflags ? flags[k] : 0u;
+  const uint32_t t = flag_type(w);
+  const bool simple = k < nflags && (w & kMaskBits) == kMaskBits && (t == FLUID || t == BOUNCE_BACK_WALL);
+  const unsigned all = __ballot_sync(0xffffffffu, simple);
+  if ((threadIdx.x & 31) == 0 && all == 0xffffffffu) atomicOr(ubits + (k >> 10), 1u << ((k >> 5) & 31));
+}
+
 // live-brick masks: bit b of tile t is set iff brick b holds a non-solid node
 __global__ void k_brick_mask(uint32_t* __restrict__ bmask, const uint32_t* __restrict__ flags, Geo g,
                              long long nslots) {
@@ -552,6 +565,7 @@ __device__ __forceinline__ void zero_fill(const Planes<T>& P, int s) {
 
 template <typename T, int MODE, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
+                                                   const uint32_t* __restrict__ ubits,
                                                    const T* __restrict__ bcv,
                                                    const T* __restrict__ bcr, Geo g, T om,
                                                    const Halo<T> H) {
@@ -560,7 +574,8 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
   const int fi = (z * g.ny + y) * g.nxp + x;
   const int s = fi + (int)g.plane;
-  const uint32_t w = __ldg(flags + fi);
+  const uint32_t ub = __ldg(ubits + (fi >> 10));
+  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
   const bool live = flag_type(w) != SOLID;
   const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
   const uint32_t miss = ~w & kMaskBits;
@@ -736,6 +751,9 @@ struct lbm_handle {
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
+  uint32_t* ubits = nullptr;  // dense: uniform-chunk bitmap (1 bit per 32 nodes)
+  bool use_ubits = true;
+  long long meta_bytes = 0;   // flag / index bytes one step reads
   void* bcv = nullptr;    // (nb, 3) storage type
   void* bcr = nullptr;    // (nb) storage type
   uint8_t* bckind64 = nullptr;
@@ -825,6 +843,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->tiles);
   dev_free(h->nbr27);
   dev_free(h->bmask);
+  dev_free(h->ubits);
   dev_free(h->bcv);
   dev_free(h->bcr);
   dev_free(h->bckind64);
@@ -834,6 +853,7 @@ void free_geometry(lbm_handle* h) {
   h->flags = nullptr;
   h->rank = h->tiles = h->nbr27 = nullptr;
   h->bmask = nullptr;
+  h->ubits = nullptr;
   h->bcv = h->bcr = nullptr;
   h->bckind64 = nullptr;
   h->bcv64 = h->bcr64 = nullptr;
@@ -921,13 +941,13 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
     dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
     const Halo<T> H = make_halo<T>(h, 1 - h->parity);
     if (var == 1)
-      k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
+      k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
     else if (var == 2)
-      k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
+      k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
     else if (var == 3)
-      k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
+      k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
     else
-      k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, bv, br, g, om, H);
+      k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
   } else {
     if (h->n_tiles == 0) return 0;
     switch (g.tn) {
@@ -1002,6 +1022,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     g.zero_fill = (zf && zf[0] == '0') ? 0 : 1;
     const char* sv = getenv("LBM_STEP_VARIANT");
     h->variant = sv ? atoi(sv) : 0;
+    const char* ub = getenv("LBM_UBITS");
+    h->use_ubits = !(ub && ub[0] == '0');
     const char* gv = getenv("LBM_GRAPH");
     h->use_graph = !(gv && gv[0] == '0');
   }
@@ -1160,6 +1182,22 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       k_flags_dense<<<grid, 128, 0, h->stream>>>(h->flags, dtype_, dorient, dbc, glo, ghi, g, nb, derr,
                                                  h->uscratch);
       CKL();
+      const long long nwords = (h->nflags + 1023) / 1024;
+      if ((rc = dev_alloc(h, &h->ubits, nwords * 4))) goto done;
+      CK(cudaMemsetAsync(h->ubits, 0, nwords * 4, h->stream));
+      if (h->use_ubits) {
+        k_uniform_bits<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(h->ubits, h->flags, h->nflags);
+        CKL();
+      }
+      {
+        std::vector<uint32_t> hb(nwords);
+        CK(cudaMemcpyAsync(hb.data(), h->ubits, nwords * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        long long uni = 0;
+        for (uint32_t v : hb) uni += __builtin_popcount(v);
+        // the step reads the bitmap plus the flag words of non-uniform chunks
+        h->meta_bytes = nwords * 4 + (h->nflags - 32 * uni) * 4;
+      }
     } else {
       const long long G = h->ntiles_grid;
       if ((rc = dev_alloc(h, &h->rank, G * 4)) || (rc = dev_alloc(h, &keep, G * 4)) ||
@@ -1203,6 +1241,16 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       if (h->nflags > 0) {
         k_brick_mask<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(h->bmask, h->flags, g, h->nflags);
         CKL();
+      }
+      {
+        std::vector<uint32_t> hb((T > 0 ? T : 1) * 4);
+        CK(cudaMemcpyAsync(hb.data(), h->bmask, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        long long bricks = 0;
+        for (uint32_t v : hb) bricks += __builtin_popcount(v);
+        const int bn = 1 << (g.lbx + g.lby + g.lbz);
+        // per tile: nbr27 + brick mask; per live brick: its flag words
+        h->meta_bytes = T * (27 * 4 + 16) + bricks * bn * 4;
       }
       h->sm.rank = h->rank;
     }
@@ -1597,6 +1645,7 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->device_bytes = h->device_bytes;
   s->launches_total = h->launches;
   s->last_step_ms = h->last_ms;
+  s->meta_bytes_per_step = h->meta_bytes;
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
   return 0;
