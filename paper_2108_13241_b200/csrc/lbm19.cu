@@ -274,13 +274,24 @@ __global__ void k_uniform_bits(uint32_t* __restrict__ ubits, const uint32_t* __r
 }
 
 // live-brick masks: bit b of tile t is set iff brick b holds a non-solid node
+// words 0-3 of a tile: live bricks; words 4-7: uniform bricks (every node
+// FLUID / BOUNCE_BACK_WALL with a full mask: the step skips their flag words)
 __global__ void k_brick_mask(uint32_t* __restrict__ bmask, const uint32_t* __restrict__ flags, Geo g,
-                             long long nslots) {
-  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nslots || flag_type(flags[s]) == SOLID) return;
-  const long long t = s >> g.ltn;
-  const int b = (int)(s & (g.tn - 1)) >> (g.lbx + g.lby + g.lbz);
-  atomicOr(bmask + 4 * t + (b >> 5), 1u << (b & 31));
+                             long long nbricks) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nbricks) return;
+  const int lbn = g.lbx + g.lby + g.lbz;
+  const long long t = k >> (g.ltn - lbn);
+  const int b = (int)(k & ((g.tn >> lbn) - 1));
+  bool live = false, uni = true;
+  for (int r = 0; r < (1 << lbn); ++r) {
+    const uint32_t w = flags[(k << lbn) + r];
+    const uint32_t ty = flag_type(w);
+    live |= ty != SOLID;
+    uni &= (w & kMaskBits) == kMaskBits && (ty == FLUID || ty == BOUNCE_BACK_WALL);
+  }
+  if (live) atomicOr(bmask + 8 * t + (b >> 5), 1u << (b & 31));
+  if (uni) atomicOr(bmask + 8 * t + 4 + (b >> 5), 1u << (b & 31));
 }
 
 // ------------------------------------------------------------ init / readback
@@ -643,7 +654,9 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
   // holding >= 1 non-solid node, a 128-bit mask per tile), so a sparse tile
   // costs lanes in proportion to its live sectors, not its 512 slots
   const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  uint32_t m[4] = {0u, 0u, 0u, 0u};
+  uint32_t m[4] = {0u, 0u, 0u, 0u}, u[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) u[q] = __ldg(bmask + 8LL * t + 4 + q);
   int pre_cnt[4] = {0, 0, 0, 0};
   int work = TN;
   bool dense_tile = true;
@@ -651,7 +664,7 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
     int acc = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      m[q] = __ldg(bmask + 4LL * t + q);
+      m[q] = __ldg(bmask + 8LL * t + q);
       pre_cnt[q] = acc;
       acc += __popc(m[q]);
     }
@@ -676,7 +689,11 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
       const int b = in ? q * 32 + (int)pos : 0;
       l = (b << lbn) | (k & (bn - 1));
     }
-    const uint32_t w = in ? __ldg(flags + (size_t)t * TN + l) : 0u;
+    const int bb = l >> lbn;
+    const uint32_t uq = bb < 32 ? u[0] : (bb < 64 ? u[1] : (bb < 96 ? u[2] : u[3]));
+    const bool uniform = in && ((uq >> (bb & 31)) & 1u);
+    const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0)
+                               : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
     const bool live = flag_type(w) != SOLID;
     const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
     if (!live) {
@@ -1236,21 +1253,23 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
             h->flags, h->tiles, dtype_, dorient, dbc, glo, ghi, g, h->nflags, nb, derr, h->uscratch);
         CKL();
       }
-      if ((rc = dev_alloc(h, &h->bmask, (T > 0 ? T : 1) * 16))) goto done;
-      CK(cudaMemsetAsync(h->bmask, 0, (T > 0 ? T : 1) * 16, h->stream));
-      if (h->nflags > 0) {
-        k_brick_mask<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(h->bmask, h->flags, g, h->nflags);
+      if ((rc = dev_alloc(h, &h->bmask, (T > 0 ? T : 1) * 32))) goto done;
+      CK(cudaMemsetAsync(h->bmask, 0, (T > 0 ? T : 1) * 32, h->stream));
+      const int bn = 1 << (g.lbx + g.lby + g.lbz);
+      const long long nbricks = h->nflags / bn;
+      if (nbricks > 0) {
+        k_brick_mask<<<(unsigned)((nbricks + 255) / 256), 256, 0, h->stream>>>(h->bmask, h->flags, g, nbricks);
         CKL();
       }
+      if (!h->use_ubits) CK(cudaMemset2DAsync(h->bmask + 4, 32, 0, 16, (T > 0 ? T : 1), h->stream));
       {
-        std::vector<uint32_t> hb((T > 0 ? T : 1) * 4);
+        std::vector<uint32_t> hb((T > 0 ? T : 1) * 8);
         CK(cudaMemcpyAsync(hb.data(), h->bmask, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        long long bricks = 0;
-        for (uint32_t v : hb) bricks += __builtin_popcount(v);
-        const int bn = 1 << (g.lbx + g.lby + g.lbz);
-        // per tile: nbr27 + brick mask; per live brick: its flag words
-        h->meta_bytes = T * (27 * 4 + 16) + bricks * bn * 4;
+        long long live = 0, uni = 0;
+        for (size_t k = 0; k < hb.size(); ++k) (k % 8 < 4 ? live : uni) += __builtin_popcount(hb[k]);
+        // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag words
+        h->meta_bytes = T * (27 * 4 + 32) + (live - uni) * bn * 4;
       }
       h->sm.rank = h->rank;
     }
