@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MLUPS per GPU and whole box (1/2/4/8 B200) and % of HBM roofline vs CPU ref"
+DEFAULT_SCHEME = "ab"
 BYTES_PER_NODE_F32 = 19 * 4 * 2 + 4     # with one flag word per node
 PDF_BYTES_PER_NODE_F32 = 19 * 4 * 2
 
@@ -89,6 +90,12 @@ def build_workload(name, rank=0, world=1):
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
         desc = "C4: D3Q19 vascular tube forest 1024^3, ~5% non-solid, pointer-tile 8^3, fp32"
         return geom, params, "pointer_tile", desc, 1.0
+    if name == "c5":
+        geom = lb.build_duct_z(1024, 1024, 2048)
+        params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
+        desc = ("C5 whole domain on one GPU: D3Q19 duct 1024x1024x2048 along z, velocity inlet "
+                "z=0, pressure outlet z=2047, bounce-back x/y faces, fp32 (needs the AA scheme)")
+        return geom, params, "dense", desc, 1.0
     if name == "duct":
         geom = lb.build_duct_z(1024, 1024, 256)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
@@ -235,6 +242,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
+    ap.add_argument("--scheme", default=None, choices=["ab", "aa"],
+                    help="PDF storage: two buffers (ab) or one in place (aa)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variants", default=None,
@@ -257,6 +266,7 @@ def main():
     import paper_2108_13241_b200 as lb
     workload = args.workload or "channel512"
     geom, params, layout, desc, rho0 = build_workload(workload)
+    scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
     if args.variants:
         for v in args.variants.split(","):
             # "3" selects LBM_STEP_VARIANT=3; "KEY=VAL;KEY=VAL" sets library switches
@@ -266,7 +276,8 @@ def main():
                     os.environ[k] = val
             else:
                 os.environ["LBM_STEP_VARIANT"] = v
-            sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
+            sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
+                                scheme=scheme)
             sim.initialize(rho0)
             sim.step(args.warmup)
             sim.step(args.steps)
@@ -281,7 +292,7 @@ def main():
                               "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
         return
-    sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
+    sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local, scheme=scheme)
     sim.initialize(rho0)
     sim.step(args.warmup)
     launches0 = sim.launches_total
@@ -310,17 +321,21 @@ def main():
         d = geom.descriptors
         h2d = d.type_tag.nbytes + d.orientation.nbytes + d.bc_index.nbytes
         nx, ny, nz = geom.dims
-        d2h = 4 * 8 * nx * ny * nz
+        # result read back: (rho, u) in f64, or rho alone past 2^30 nodes (host RAM)
+        big = nx * ny * nz > (1 << 30)
+        d2h = (1 if big else 4) * 8 * nx * ny * nz
         t0 = time.perf_counter()
-        s2 = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local)
+        s2 = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
+                           scheme=scheme)
         s2.initialize(rho0)
         s2.step(args.steps)
-        fields = s2.macroscopic_fields()
+        fields = s2.density_field() if big else s2.macroscopic_fields()
         t1 = time.perf_counter()
         e2e = {"value": nons * args.steps / (t1 - t0) / 1e6, "unit": "MLUPS",
                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                "what": "Simulation(geometry) [descriptor upload] + initialize + step(K) + "
-                       "macroscopic_fields() [f64 rho,u readback], wall clock"}
+                       + ("density_field() [f64 rho readback]" if big else
+                          "macroscopic_fields() [f64 rho,u readback]") + ", wall clock"}
         del fields
         s2.close()
 
@@ -335,7 +350,7 @@ def main():
         "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "layout": layout, "nodes": int(st.n_nodes),
+        "config": {"workload": desc, "layout": layout, "scheme": scheme, "nodes": int(st.n_nodes),
                    "non_solid_nodes": int(nons), "tiles": int(st.n_tiles),
                    "l2": "state 2x19 planes >> 126 MB L2 (no flush needed)",
                    "parallelism": "single GPU"},

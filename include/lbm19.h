@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define LBM_ABI_VERSION 1
+#define LBM_ABI_VERSION 2
 
 enum {
   LBM_OK = 0,
@@ -65,6 +65,15 @@ enum {
   LBM_LAYOUT_POINTER_TILE = 3  /* compacted tile list + nbr27 (sparse) */
 };
 
+/* distribution storage scheme (orthogonal to the layout).  The reference
+ * keeps two buffers and swaps them (layouts.py:309-310): LBM_SCHEME_AB.
+ * LBM_SCHEME_AA keeps ONE buffer updated in place by alternating a
+ * neighbour step (pull from x - c_i, push to x + c_i) and a node-local step;
+ * it halves the PDF memory at the same 152 B/node traffic and gives results
+ * bit-identical to AB.  Readbacks decode it (`pre` is always the reference's
+ * pre buffer); there is no `post` buffer under AA. */
+enum { LBM_SCHEME_AB = 0, LBM_SCHEME_AA = 1 };
+
 typedef struct lbm_desc {
   int32_t nx, ny, nz;     /* extents of THIS handle's nodes (nz = slab planes) */
   int32_t nz_global;      /* global z extent (== nz on one device) */
@@ -75,6 +84,7 @@ typedef struct lbm_desc {
   int32_t tile[3];        /* tile edge lengths for tile layouts (default 8,8,8) */
   int32_t device;         /* CUDA device ordinal */
   double omega;           /* BGK collision frequency, cast to dtype */
+  int32_t scheme;         /* LBM_SCHEME_AB (two buffers) / LBM_SCHEME_AA (one, in place) */
 } lbm_desc;
 
 typedef struct lbm_stats {
@@ -90,8 +100,9 @@ typedef struct lbm_stats {
   int64_t launches_total;   /* kernels launched by lbm_step so far */
   double last_step_ms;      /* device time of the last lbm_step call (CUDA events) */
   int64_t meta_bytes_per_step; /* flag / index bytes the step kernel reads per step */
-  int32_t parity;
+  int32_t parity;           /* AB: index of the pre buffer; AA: step phase (step_count mod 2) */
   int32_t initialized;
+  int32_t scheme;           /* LBM_SCHEME_* */
 } lbm_stats;
 
 typedef struct lbm_handle lbm_t;
@@ -134,11 +145,14 @@ int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz);
 int lbm_total_mass(lbm_t* h, double* mass);
 
 /* which: 0 = pre, 1 = post.  Canonical (19, nz, ny, nx) in the handle dtype;
- * nodes without storage read 0 (set_pdf ignores them). */
+ * nodes without storage read 0 (set_pdf ignores them).  Under LBM_SCHEME_AA
+ * `pre` is decoded from the in-place buffer and which = 1 is LBM_EINVAL. */
 int lbm_get_pdf(lbm_t* h, int32_t which, void* out);
 int lbm_set_pdf(lbm_t* h, int32_t which, const void* in);
 /* Native storage, 19 * plane_stride elements in the handle dtype: dense
- * (19, plane_stride) SoA; tile layouts AoSoA (n_tiles, 19, tile nodes). */
+ * (19, plane_stride) SoA; tile layouts AoSoA (n_tiles, 19, tile nodes).
+ * Under LBM_SCHEME_AA which = 0 is the decoded pre buffer in the same native
+ * order (slots without a non-solid node read 0) and which = 1 is LBM_EINVAL. */
 int lbm_get_field(lbm_t* h, int32_t which, void* out);
 int lbm_set_field(lbm_t* h, int32_t which, const void* in);
 /* slot of each node (nz, ny, nx), -1 when the node has no storage. */

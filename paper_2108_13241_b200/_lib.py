@@ -17,6 +17,8 @@ LBM_OK, LBM_EINVAL, LBM_ESTATE, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EDIVERGED 
     0, -1, -2, -3, -4, -5, -6
 LBM_F32, LBM_F64 = 0, 1
 LAYOUT_CODES = {"dense": 0, "tile": 1, "bitmask_node": 2, "pointer_tile": 3}
+SCHEME_CODES = {"ab": 0, "aa": 1}
+ABI_VERSION = 2
 HALO_BLOB_BYTES = 512
 
 
@@ -25,7 +27,7 @@ class LbmDesc(C.Structure):
                 ("nz_global", C.c_int32), ("z0", C.c_int32),
                 ("periodic", C.c_int32 * 3), ("dtype", C.c_int32),
                 ("layout", C.c_int32), ("tile", C.c_int32 * 3),
-                ("device", C.c_int32), ("omega", C.c_double)]
+                ("device", C.c_int32), ("omega", C.c_double), ("scheme", C.c_int32)]
 
 
 class LbmStats(C.Structure):
@@ -36,7 +38,7 @@ class LbmStats(C.Structure):
                 ("device_bytes", C.c_int64), ("launches_total", C.c_int64),
                 ("last_step_ms", C.c_double), ("meta_bytes_per_step", C.c_int64),
                 ("parity", C.c_int32),
-                ("initialized", C.c_int32)]
+                ("initialized", C.c_int32), ("scheme", C.c_int32)]
 
 
 P = C.c_void_p
@@ -102,7 +104,7 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.lbm_abi_version() != 1:
+    if lib.lbm_abi_version() != ABI_VERSION:
         raise ImportError("liblbm19.so ABI version mismatch; rebuild it")
     _lib = lib
     return lib

@@ -23,6 +23,7 @@
 //          block contiguous (8^3 fp32 -> 2 KB).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <cstdarg>
@@ -79,6 +80,8 @@ struct Geo {
   int tn;                  // nodes per tile
   int ltn;                 // log2(tn)
   int zero_fill;           // complete mixed sectors with zeros (full-sector stores)
+  int aa;                  // LBM_SCHEME_AA: one buffer updated in place
+  int aph;                 // AA state phase (step_count mod 2), set per readback launch
 };
 
 // In-tile slot order: the tile is cut into bricks of one 32-byte sector
@@ -126,7 +129,31 @@ struct SlotMap {
   __device__ __forceinline__ long long flag_index(const Geo& g, long long s) const {
     return g.tiled ? s : s - g.plane;
   }
+  // slot of the neighbour x + c_i of a node whose link i is present (so the
+  // neighbour is inside the domain or across a periodic face)
+  __device__ __forceinline__ long long nbr_slot(const Geo& g, int x, int y, int z, int i) const {
+    x += cx(i);
+    y += cy(i);
+    z += cz(i);
+    if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;
+    if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
+    if (g.pzw) { if (z < 0) z += g.nz; else if (z >= g.nz) z -= g.nz; }
+    return slot(g, x, y, z);
+  }
 };
+
+// Where pre_i(x) of the reference lives (element index into the buffer).
+// AB: the pre buffer itself.  AA (one buffer F, in place):
+//   phase 0 (even step count): pre_i(x) = F[opp(i)][x]
+//   phase 1 (odd):             pre_i(x) = F[i][x + c_i] if link i of x is
+//                              present, else F[opp(i)][x]
+// (see k_step_dense_aa for the two steps that produce these states).
+__device__ __forceinline__ long long pre_index(const Geo& g, const SlotMap& sm, int i, long long s,
+                                               uint32_t w, int x, int y, int z) {
+  if (!g.aa || i == 0) return fidx(g, i, s);
+  if (g.aph && ((w >> (i - 1)) & 1u)) return fidx(g, i, sm.nbr_slot(g, x, y, z, i));
+  return fidx(g, opp(i), s);
+}
 
 // --------------------------------------------------------------- geometry
 __device__ __forceinline__ uint32_t type_at(const uint8_t* __restrict__ type,
@@ -237,6 +264,28 @@ __global__ void k_tile_nbr(int* __restrict__ nbr, const int* __restrict__ tiles,
   nbr[k] = v;
 }
 
+// Morton key of each kept tile (x, y, z bits interleaved), sorted to a launch
+// order: 3-D neighbours of a tile then run close in time, so the sectors they
+// share (pulled across tile faces, or pushed by the AA neighbour step) are
+// still in L2 when the second CTA touches them.  The rank order itself --
+// the reference's row-major pointer-tile order -- is unchanged.
+__device__ __forceinline__ unsigned long long spread3(unsigned v) {
+  unsigned long long x = v & 0x1fffffu;
+  x = (x | x << 32) & 0x1f00000000ffffULL;
+  x = (x | x << 16) & 0x1f0000ff0000ffULL;
+  x = (x | x << 8) & 0x100f00f00f00f00fULL;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+  x = (x | x << 2) & 0x1249249249249249ULL;
+  return x;
+}
+__global__ void k_tile_morton(unsigned long long* __restrict__ key, int* __restrict__ val,
+                              const int* __restrict__ tiles, long long T) {
+  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= T) return;
+  key[r] = spread3(tiles[3 * r]) | spread3(tiles[3 * r + 1]) << 1 | spread3(tiles[3 * r + 2]) << 2;
+  val[r] = (int)r;
+}
+
 // tiles: one thread per slot of the kept tiles
 __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict__ tiles,
                              const uint8_t* __restrict__ type, const uint8_t* __restrict__ orient,
@@ -319,24 +368,27 @@ __global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, 
   } else if (t == PRESSURE_BC && b < nb && bckind[b] == 1) {
     r = bcr[b];
   }
+  // AA starts in phase 0: pre_i(x) sits at F[opp(i)][x]
 #pragma unroll
-  for (int i = 0; i < Q; ++i) pre[fidx(g, i, s)] = (T)init_eq(i, r, vx, vy, vz);
+  for (int i = 0; i < Q; ++i) pre[fidx(g, g.aa ? opp(i) : i, s)] = (T)init_eq(i, r, vx, vy, vz);
 }
 
 template <typename T>
 __global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
-                        Geo g, double* __restrict__ rho, double* __restrict__ ux,
+                        Geo g, int z0, double* __restrict__ rho, double* __restrict__ ux,
                         double* __restrict__ uy, double* __restrict__ uz) {
+  // planes z0 .. z0 + gridDim.z - 1 into a staging chunk
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int y = blockIdx.y, z = blockIdx.z + z0;
   if (x >= g.nx) return;
-  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
   const long long s = sm.slot(g, x, y, z);
   double r = 0, vx = 0, vy = 0, vz = 0;
-  if (s >= 0 && flag_type(flags[sm.flag_index(g, s)]) != SOLID) {
+  const uint32_t w = s >= 0 ? flags[sm.flag_index(g, s)] : 0u;
+  if (s >= 0 && flag_type(w) != SOLID) {
     double f[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = (double)pre[fidx(g, i, s)];
+    for (int i = 0; i < Q; ++i) f[i] = (double)pre[pre_index(g, sm, i, s, w, x, y, z)];
     using A = ar<double>;
     r = density19(f);
     if (r != 0.0) {
@@ -354,28 +406,62 @@ __global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ 
 }
 
 template <typename T>
-__global__ void k_get_pdf(const T* __restrict__ buf, SlotMap sm, Geo g, T* __restrict__ out) {
+__global__ void k_get_pdf(const T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
+                          int z0, T* __restrict__ out) {
+  // planes z0 .. z0 + gridDim.z - 1 into a (19, chunk nodes) staging block
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int y = blockIdx.y, z = blockIdx.z + z0;
   if (x >= g.nx) return;
-  const long long N = (long long)g.nx * g.ny * g.nz;
-  const long long n = ((long long)z * g.ny + y) * g.nx + x;
+  const long long N = (long long)g.nx * g.ny * gridDim.z;
+  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
   const long long s = sm.slot(g, x, y, z);
+  if (s < 0) {
 #pragma unroll
-  for (int i = 0; i < Q; ++i) out[i * N + n] = s >= 0 ? buf[fidx(g, i, s)] : (T)0;
+    for (int i = 0; i < Q; ++i) out[i * N + n] = (T)0;
+    return;
+  }
+  const uint32_t w = flags[sm.flag_index(g, s)];
+  // AA holds only non-solid nodes' values; solid storage reads 0 either way
+  const bool live = !g.aa || flag_type(w) != SOLID;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) out[i * N + n] = live ? buf[pre_index(g, sm, i, s, w, x, y, z)] : (T)0;
 }
 
 template <typename T>
-__global__ void k_set_pdf(T* __restrict__ buf, SlotMap sm, Geo g, const T* __restrict__ in) {
+__global__ void k_set_pdf(T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
+                          int z0, const T* __restrict__ in) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z + z0;
+  if (x >= g.nx) return;
+  const long long N = (long long)g.nx * g.ny * gridDim.z;
+  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
+  const long long s = sm.slot(g, x, y, z);
+  if (s < 0) return;
+  const uint32_t w = flags[sm.flag_index(g, s)];
+  if (g.aa && flag_type(w) == SOLID) return;  // AA: solid storage is never written
+#pragma unroll
+  for (int i = 0; i < Q; ++i) buf[pre_index(g, sm, i, s, w, x, y, z)] = in[i * N + n];
+}
+
+// AA: decoded pre buffer in the native slot order (lbm_get_field / set_field)
+template <typename T, bool GET>
+__global__ void k_field_aa(T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
+                           T* __restrict__ io) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nx) return;
-  const long long N = (long long)g.nx * g.ny * g.nz;
-  const long long n = ((long long)z * g.ny + y) * g.nx + x;
   const long long s = sm.slot(g, x, y, z);
   if (s < 0) return;
+  const uint32_t w = flags[sm.flag_index(g, s)];
+  if (flag_type(w) == SOLID) return;
 #pragma unroll
-  for (int i = 0; i < Q; ++i) buf[fidx(g, i, s)] = in[i * N + n];
+  for (int i = 0; i < Q; ++i) {
+    const long long k = pre_index(g, sm, i, s, w, x, y, z);
+    if (GET)
+      io[fidx(g, i, s)] = buf[k];
+    else
+      buf[k] = io[fidx(g, i, s)];
+  }
 }
 
 __global__ void k_slot_of(SlotMap sm, Geo g, int* __restrict__ out) {
@@ -403,10 +489,12 @@ __global__ void k_nonfinite(const T* __restrict__ pre, const uint32_t* __restric
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nx) return;
   const long long s = sm.slot(g, x, y, z);
-  if (s < 0 || flag_type(flags[sm.flag_index(g, s)]) == SOLID) return;
+  if (s < 0) return;
+  const uint32_t w = flags[sm.flag_index(g, s)];
+  if (flag_type(w) == SOLID) return;
   const long long v = g.tiled ? s : ((long long)z * g.ny + y) * g.nx + x;
   for (int i = 0; i < Q; ++i) {
-    const T val = pre[fidx(g, i, s)];
+    const T val = pre[pre_index(g, sm, i, s, w, x, y, z)];
     if (!isfinite((double)val)) {
       atomicMin(best, (unsigned long long)(i * V + v));
       return;
@@ -416,16 +504,33 @@ __global__ void k_nonfinite(const T* __restrict__ pre, const uint32_t* __restric
 
 // deterministic two-pass mass reduction: per-block partial sums, then one block
 template <typename T>
-__global__ void k_mass_partial(const T* __restrict__ pre, const uint32_t* __restrict__ flags, Geo g,
-                               long long nflags, double* __restrict__ partial) {
+__global__ void k_mass_partial(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
+                               const int* __restrict__ tiles, Geo g, long long nflags,
+                               double* __restrict__ partial) {
   __shared__ double sh[256];
   double acc = 0.0;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nflags;
        k += (long long)gridDim.x * blockDim.x) {
-    if (flag_type(flags[k]) == SOLID) continue;
+    const uint32_t w = flags[k];
+    if (flag_type(w) == SOLID) continue;
     const long long s = g.tiled ? k : k + g.plane;
+    int x = 0, y = 0, z = 0;  // node coordinates (AA phase 1 reads neighbours)
+    if (g.aa && g.aph) {
+      if (g.tiled) {
+        const long long t = k >> g.ltn;
+        brick_inv(g, (int)(k & (g.tn - 1)), x, y, z);
+        x += tiles[3 * t] * g.ex;
+        y += tiles[3 * t + 1] * g.ey;
+        z += tiles[3 * t + 2] * g.ez;
+      } else {
+        z = (int)(k / g.plane);
+        const long long r = k - (long long)z * g.plane;
+        y = (int)(r / g.nxp);
+        x = (int)(r - (long long)y * g.nxp);
+      }
+    }
     double a = 0.0;
-    for (int i = 0; i < Q; ++i) a += (double)pre[fidx(g, i, s)];
+    for (int i = 0; i < Q; ++i) a += (double)pre[pre_index(g, sm, i, s, w, x, y, z)];
     acc += a;
   }
   sh[threadIdx.x] = acc;
@@ -521,9 +626,8 @@ struct Planes {
 };
 
 template <typename T>
-__device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
-                                                 const T* __restrict__ bcr, T om,
-                                                 const Planes<T>& P, int s) {
+__device__ __forceinline__ void bc_collide(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
+                                           const T* __restrict__ bcr, T om) {
   const uint32_t t = flag_type(w);
   if (t == VELOCITY_BC) {
     const uint32_t b = flag_bc(w);
@@ -534,6 +638,13 @@ __device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T*
   T rho, vx, vy, vz;
   moments19(f, rho, vx, vy, vz);
   collide19(f, rho, vx, vy, vz, om);
+}
+
+template <typename T>
+__device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
+                                                 const T* __restrict__ bcr, T om,
+                                                 const Planes<T>& P, unsigned s) {
+  bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
   for (int i = 0; i < Q; ++i) P.post[i][s] = f[i];
 }
@@ -542,7 +653,7 @@ __device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T*
 // upstream slot (always a valid address); where the mask bit of opp(i) is
 // clear the node reflects its own f_opp(i) instead (reference kernel.py:84-116).
 template <typename T>
-__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, const Planes<T>& P, int s) {
+__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, const Planes<T>& P, unsigned s) {
   if (miss) {
 #pragma unroll
     for (int i = 1; i < Q; ++i)
@@ -555,7 +666,7 @@ __device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, cons
 // nodes all have full masks pull unconditionally, the others select per link
 // so no byte is fetched for a masked link.
 template <typename T, int MODE, typename Up>
-__device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, const Planes<T>& P, int s,
+__device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, const Planes<T>& P, unsigned s,
                                        Up up) {
   if (MODE == 0 || fast) {
 #pragma unroll
@@ -569,10 +680,31 @@ __device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, cons
 }
 
 template <typename T>
-__device__ __forceinline__ void zero_fill(const Planes<T>& P, int s) {
+__device__ __forceinline__ void zero_fill(const Planes<T>& P, unsigned s) {
 #pragma unroll
   for (int i = 0; i < Q; ++i) P.post[i][s] = (T)0;
 }
+
+// dense: offsets from slot s to the upstream node x - c_i, per axis (wrap on
+// periodic axes; on closed axes the edge offset is 0 and the link is masked,
+// so the speculative address stays valid)
+struct UpOffsets {
+  unsigned xm, xp, ym, yp, zm, zp;
+  __device__ __forceinline__ UpOffsets(const Geo& g, int x, int y, int z) {
+    xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
+    xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
+    ym = y == 0 ? (g.py ? (unsigned)(g.ny - 1) * g.nxp : 0u) : (unsigned)-g.nxp;
+    yp = y == g.ny - 1 ? (g.py ? (unsigned)-((g.ny - 1) * g.nxp) : 0u) : (unsigned)g.nxp;
+    const unsigned pl = (unsigned)g.plane;
+    zm = (z == 0 && g.pzw) ? (unsigned)(g.nz - 1) * pl : 0u - pl;
+    zp = (z == g.nz - 1 && g.pzw) ? 0u - (unsigned)(g.nz - 1) * pl : pl;
+  }
+  // slot of x - c_i
+  __device__ __forceinline__ unsigned up(unsigned s, int i) const {
+    return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0u)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0u)) +
+           (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0u));
+  }
+};
 
 template <typename T, int MODE, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
@@ -583,8 +715,10 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
-  const int fi = (z * g.ny + y) * g.nxp + x;
-  const int s = fi + (int)g.plane;
+  // 32-bit unsigned slot arithmetic (slabs up to 2^32 slots; negative
+  // offsets wrap modulo 2^32 and land on the right slot)
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
+  const unsigned s = fi + (unsigned)g.plane;
   const uint32_t ub = __ldg(ubits + (fi >> 10));
   const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
   const bool live = flag_type(w) != SOLID;
@@ -599,17 +733,8 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   }
   // offsets to the upstream node x - c_i along each axis (wrap on periodic
   // axes; on closed axes the edge offset is 0 and the link is masked)
-  const int xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
-  const int xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
-  const int ym = y == 0 ? (g.py ? (g.ny - 1) * g.nxp : 0) : -g.nxp;
-  const int yp = y == g.ny - 1 ? (g.py ? -(g.ny - 1) * g.nxp : 0) : g.nxp;
-  const int pl = (int)g.plane;
-  const int zm = (z == 0 && g.pzw) ? (g.nz - 1) * pl : -pl;
-  const int zp = (z == g.nz - 1 && g.pzw) ? -(g.nz - 1) * pl : pl;
-  auto up = [&](int i) {
-    return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0)) +
-           (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0));
-  };
+  const UpOffsets o(g, x, y, z);
+  auto up = [&](int i) { return o.up(s, i); };
   T f[Q];
   f[0] = __ldg(P.pre[0] + s);
   gather<T, MODE>(f, miss, fast, P, s, up);
@@ -628,72 +753,205 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   }
 }
 
+// A-A in place (LBM_SCHEME_AA): one buffer F, two alternating kernels, each
+// node reading and writing only locations no other node touches in the same
+// launch, so no second buffer is needed.  Per reference step (pull gather of
+// the previous post-collision values, then collide; kernel.py:72-141):
+//   NB = 1 (state phase 0 -> 1), F[opp(i)][x] holds pre_i(x):
+//      f_i = F[opp(i)][x - c_i]  if link opp(i) of x is present (pre_i(x - c_i))
+//          = F[i][x]             otherwise (bounce-back: pre_opp(i)(x))
+//      store f*_i to F[i][x + c_i] if link i is present, else F[opp(i)][x]
+//   NB = 0 (phase 1 -> 0): f_i = F[i][x]; store f*_i to F[opp(i)][x]
+// F[i][x + c_i] is read (as f_opp(i)) and written by node x alone, so the
+// update is race-free; the arithmetic is the AB kernel's, bit for bit.
+template <typename T>
+struct Planes1 {
+  T* f[Q];
+};
+
+// AA loads may take the read-only (non-coherent) path: every location is
+// read and then written by one thread only, so no cached copy can be stale
+template <typename T>
+__device__ __forceinline__ T LDA(const T* p) {
+  return __ldg(p);
+}
+
+// hides a value from the optimiser: the neighbour step's store addresses are
+// the load addresses of the opposite directions, and letting the compiler
+// keep those 18 addresses live across the collision costs spills; an opaque
+// copy makes it recompute them from a handful of offsets instead
+__device__ __forceinline__ unsigned opaque(unsigned v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ int opaque(int v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+
+template <typename T, int NB, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P, const uint32_t* __restrict__ flags,
+                                                      const uint32_t* __restrict__ ubits,
+                                                      const T* __restrict__ bcv, const T* __restrict__ bcr,
+                                                      Geo g, T om) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nxp) return;
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
+  const unsigned s = fi + (unsigned)g.plane;
+  const uint32_t ub = __ldg(ubits + (fi >> 10));
+  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  // no zero-fill of solid lanes here (unlike the AB kernel): every sector
+  // this step writes was read by the same step, so it sits in L2 whole and a
+  // partial store needs no DRAM read-for-merge; zero stores from solid lanes
+  // would instead race ahead of the live lanes' loads of the same sectors
+  if (flag_type(w) == SOLID) return;
+  const uint32_t miss = ~w & kMaskBits;
+  T f[Q];
+  f[0] = LDA(P.f[0] + s);
+  if (NB) {
+    const UpOffsets o(g, x, y, z);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));  // speculative, always a valid slot
+    if (miss) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(P.f[i] + s);
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+    // recompute the store addresses from opaque copies (measured: keeping the
+    // 18 load addresses live at 64 registers is no faster)
+    const unsigned s2 = opaque(s);
+    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
+    P.f[0][s2] = f[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      T* dst = ((miss >> (i - 1)) & 1u) ? P.f[opp(i)] + s2 : P.f[i] + o2.up(s2, opp(i));
+      *dst = f[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[i] + s);
+    bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) P.f[opp(i)][s] = f[i];
+  }
+}
+
 // Sparse tiles, AoSoA storage f[tile][i][TN]: one CTA per kept tile.  All
 // addresses are 32-bit element offsets from the CTA's own tile block; the
 // upstream slot of direction i is separable per axis (tile code
 // (dx+1) + 3(dy+1) + 9(dz+1), relative tile offset from shared memory, and
 // in-tile offset lx' + ex ly' + ex ey lz'), and every own-tile access
 // (bounce-back, stores) has a compile-time offset i*TN.
-// MODE 0: speculative pull + fix-up; MODE 1: select per link (no masked
-// link fetches a byte).
+
+// Live-brick work list of one tile (MODE 2): threads cover only the tile's
+// live bricks (sector-sized bricks holding >= 1 non-solid node, a 128-bit
+// mask per tile), so a sparse tile costs lanes in proportion to its live
+// sectors, not its TN slots.  Words 4-7 of the mask mark uniform bricks
+// (all FLUID / wall with full masks) whose flag words the step skips.
+struct TileBricks {
+  uint32_t m[4], u[4];
+  int pre_cnt[4];
+  int work, lbn, bn;
+  bool dense_tile;
+  __device__ __forceinline__ TileBricks(const uint32_t* __restrict__ bmask, long long t, const Geo& g, int tn,
+                                        bool compact) {
+    lbn = g.lbx + g.lby + g.lbz;
+    bn = 1 << lbn;
+    int acc = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      u[q] = __ldg(bmask + 8LL * t + 4 + q);
+      m[q] = compact ? __ldg(bmask + 8LL * t + q) : 0u;
+      pre_cnt[q] = acc;
+      acc += __popc(m[q]);
+    }
+    work = compact ? ((acc << lbn) + 31) & ~31 : tn;  // whole warps; lanes past acc*bn idle
+    dense_tile = !compact || acc == (tn >> lbn);       // every brick live: identity mapping
+  }
+  // in-tile slot of work item k; `in` false for idle lanes past the last live brick
+  __device__ __forceinline__ int slot(int k, bool& in) const {
+    in = true;
+    if (dense_tile) return k;
+    const int j = k >> lbn;  // live-brick ordinal
+    in = j < pre_cnt[3] + __popc(m[3]);
+    int q = 3;
+    if (j < pre_cnt[3]) q = 2;
+    if (j < pre_cnt[2]) q = 1;
+    if (j < pre_cnt[1]) q = 0;
+    const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
+    const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
+    const uint32_t pos = __fns(mq, 0, j - pq + 1);
+    const int b = in ? q * 32 + (int)pos : 0;
+    return (b << lbn) | (k & (bn - 1));
+  }
+  // flag word of in-tile slot l (uniform bricks skip the load)
+  __device__ __forceinline__ uint32_t flag(const uint32_t* __restrict__ flags, long long t, int tn, int l,
+                                           bool in) const {
+    const int bb = l >> lbn;
+    const uint32_t uq = bb < 32 ? u[0] : (bb < 64 ? u[1] : (bb < 96 ? u[2] : u[3]));
+    const bool uniform = in && ((uq >> (bb & 31)) & 1u);
+    return uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * tn + l) : 0u);
+  }
+};
+
+// offset (from the own tile's block, excluding the direction plane) of the
+// node x - c_i: neighbour tile from the shared relative-offset table,
+// in-tile position from the separable brick order
+struct TileUp {
+  int cxm, lxm, cxp, lxp, cym, lym, cyp, lyp, czm, lzm, czp, lzp, lx0, ly0, lz0;
+  __device__ __forceinline__ TileUp(const Geo& g, int l) {
+    int lx, ly, lz;
+    brick_inv(g, l, lx, ly, lz);
+    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, in-tile offset)
+    cxm = lx == 0 ? -1 : 0, lxm = brick_x(g, lx == 0 ? g.ex - 1 : lx - 1);
+    cxp = lx == g.ex - 1 ? 1 : 0, lxp = brick_x(g, lx == g.ex - 1 ? 0 : lx + 1);
+    cym = ly == 0 ? -3 : 0, lym = brick_y(g, ly == 0 ? g.ey - 1 : ly - 1);
+    cyp = ly == g.ey - 1 ? 3 : 0, lyp = brick_y(g, ly == g.ey - 1 ? 0 : ly + 1);
+    czm = lz == 0 ? -9 : 0, lzm = brick_z(g, lz == 0 ? g.ez - 1 : lz - 1);
+    czp = lz == g.ez - 1 ? 9 : 0, lzp = brick_z(g, lz == g.ez - 1 ? 0 : lz + 1);
+    lx0 = brick_x(g, lx), ly0 = brick_y(g, ly), lz0 = brick_z(g, lz);
+  }
+  __device__ __forceinline__ int at(const int* srel, int i) const {
+    const int code = 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) +
+                     (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) + (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
+    const int loc = (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) + (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
+                    (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
+    return srel[code] + loc;
+  }
+};
+
+// stage the 27 neighbour ranks as relative element offsets (absent: 0, i.e.
+// the own tile -- such links are masked)
+template <int TN>
+__device__ __forceinline__ void stage_nbr(int* srel, const int* __restrict__ nbr27, int t) {
+  if (threadIdx.x < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
+    srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);
+  }
+}
+
+// MODE 0: speculative pull + fix-up over all TN slots; MODE 1: select per
+// link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only.
 template <typename T, int TN, int MODE, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
              const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-             const uint32_t* __restrict__ bmask) {
+             const uint32_t* __restrict__ bmask, const int* __restrict__ order) {
   constexpr int BT = TN < 256 ? TN : 256;
   __shared__ int srel[27];
-  const int t = blockIdx.x;
-  if (threadIdx.x < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
-    srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);  // absent: masked links, own tile
-  }
+  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  stage_nbr<TN>(srel, nbr27, t);
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  // MODE 2: threads cover only the tile's live bricks (sector-sized bricks
-  // holding >= 1 non-solid node, a 128-bit mask per tile), so a sparse tile
-  // costs lanes in proportion to its live sectors, not its 512 slots
-  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  uint32_t m[4] = {0u, 0u, 0u, 0u}, u[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) u[q] = __ldg(bmask + 8LL * t + 4 + q);
-  int pre_cnt[4] = {0, 0, 0, 0};
-  int work = TN;
-  bool dense_tile = true;
-  if (MODE == 2) {
-    int acc = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      m[q] = __ldg(bmask + 8LL * t + q);
-      pre_cnt[q] = acc;
-      acc += __popc(m[q]);
-    }
-    work = ((acc << lbn) + 31) & ~31;  // whole warps; lanes past acc*bn idle
-    dense_tile = acc == (TN >> lbn);   // every brick live: identity mapping
-  }
+  const TileBricks tw(bmask, t, g, TN, MODE == 2);
   __syncthreads();
 #pragma unroll 1
-  for (int k = threadIdx.x; k < work; k += BT) {
-    int l = k;
-    bool in = true;
-    if (MODE == 2 && !dense_tile) {
-      const int j = k >> lbn;  // live-brick ordinal
-      in = j < pre_cnt[3] + __popc(m[3]);
-      int q = 3;
-      if (j < pre_cnt[3]) q = 2;
-      if (j < pre_cnt[2]) q = 1;
-      if (j < pre_cnt[1]) q = 0;
-      const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
-      const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
-      const uint32_t pos = __fns(mq, 0, j - pq + 1);
-      const int b = in ? q * 32 + (int)pos : 0;
-      l = (b << lbn) | (k & (bn - 1));
-    }
-    const int bb = l >> lbn;
-    const uint32_t uq = bb < 32 ? u[0] : (bb < 64 ? u[1] : (bb < 96 ? u[2] : u[3]));
-    const bool uniform = in && ((uq >> (bb & 31)) & 1u);
-    const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0)
-                               : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
+  for (int k = threadIdx.x; k < tw.work; k += BT) {
+    bool in;
+    const int l = tw.slot(k, in);
+    const uint32_t w = tw.flag(flags, t, TN, l, in);
     const bool live = flag_type(w) != SOLID;
     const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
     if (!live) {
@@ -704,30 +962,12 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
       continue;
     }
     const uint32_t miss = ~w & kMaskBits;
-    int lx, ly, lz;
-    brick_inv(g, l, lx, ly, lz);
-    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, in-tile offset)
-    const int cxm = lx == 0 ? -1 : 0, lxm = brick_x(g, lx == 0 ? g.ex - 1 : lx - 1);
-    const int cxp = lx == g.ex - 1 ? 1 : 0, lxp = brick_x(g, lx == g.ex - 1 ? 0 : lx + 1);
-    const int cym = ly == 0 ? -3 : 0, lym = brick_y(g, ly == 0 ? g.ey - 1 : ly - 1);
-    const int cyp = ly == g.ey - 1 ? 3 : 0, lyp = brick_y(g, ly == g.ey - 1 ? 0 : ly + 1);
-    const int czm = lz == 0 ? -9 : 0, lzm = brick_z(g, lz == 0 ? g.ez - 1 : lz - 1);
-    const int czp = lz == g.ez - 1 ? 9 : 0, lzp = brick_z(g, lz == g.ez - 1 ? 0 : lz + 1);
-    const int lx0 = brick_x(g, lx), ly0 = brick_y(g, ly), lz0 = brick_z(g, lz);
-    auto up = [&](int i) {
-      const int code = 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) +
-                       (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
-                       (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
-      const int loc = (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) +
-                      (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
-                      (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
-      return srel[code] + i * TN + loc;
-    };
+    const TileUp up(g, l);
     T f[Q];
     f[0] = __ldg(tb + l);
     if (MODE != 1) {
 #pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + up(i));
+      for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + up.at(srel, i));
       if (miss) {
 #pragma unroll
         for (int i = 1; i < Q; ++i)
@@ -736,20 +976,61 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
     } else {
 #pragma unroll
       for (int i = 1; i < Q; ++i)
-        f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : up(i)));
+        f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : i * TN + up.at(srel, i)));
     }
-    const uint32_t ty = flag_type(w);
-    if (ty == VELOCITY_BC) {
-      const uint32_t b = flag_bc(w);
-      zou_he_velocity19<T>(f, flag_orient(w), bcv[3 * b], bcv[3 * b + 1], bcv[3 * b + 2]);
-    } else if (ty == PRESSURE_BC) {
-      zou_he_pressure19<T>(f, flag_orient(w), bcr[flag_bc(w)]);
-    }
-    T rho, vx, vy, vz;
-    moments19(f, rho, vx, vy, vz);
-    collide19(f, rho, vx, vy, vz, om);
+    bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
     for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+  }
+}
+
+// A-A in place over the tile list (see k_step_dense_aa for the scheme):
+// NB = 1 pulls F[opp(i)] at x - c_i and pushes to F[i] at x + c_i through
+// the neighbour table; NB = 0 is node-local.
+template <typename T, int TN, int NB, int MINB>
+__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
+k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
+                const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+                const uint32_t* __restrict__ bmask, const int* __restrict__ order) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  __shared__ int srel[27];
+  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  if (NB) stage_nbr<TN>(srel, nbr27, t);
+  T* __restrict__ tb = F + (size_t)t * (Q * TN);
+  const TileBricks tw(bmask, t, g, TN, true);
+  if (NB) __syncthreads();
+#pragma unroll 1
+  for (int k = threadIdx.x; k < tw.work; k += BT) {
+    bool in;
+    const int l = tw.slot(k, in);
+    const uint32_t w = tw.flag(flags, t, TN, l, in);
+    if (flag_type(w) == SOLID) continue;  // no zero-fill under AA (see k_step_dense_aa)
+    const uint32_t miss = ~w & kMaskBits;
+    T f[Q];
+    f[0] = LDA(tb + l);
+    if (NB) {
+      const TileUp up(g, l);
+#pragma unroll
+      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + opp(i) * TN + up.at(srel, i));
+      if (miss) {
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+          if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(tb + i * TN + l);
+      }
+      bc_collide<T>(f, w, bcv, bcr, om);
+      const int l2 = opaque(l);
+      const TileUp up2(g, l2);
+      tb[l2] = f[0];
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + up2.at(srel, opp(i))] = f[i];
+    } else {
+#pragma unroll
+      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
+      bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
+    }
   }
 }
 
@@ -767,6 +1048,8 @@ struct lbm_handle {
   int* rank = nullptr;    // tile rank grid
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
+  int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
+  bool morton = false;
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
   uint32_t* ubits = nullptr;  // dense: uniform-chunk bitmap (1 bit per 32 nodes)
   bool use_ubits = true;
@@ -859,6 +1142,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->rank);
   dev_free(h->tiles);
   dev_free(h->nbr27);
+  dev_free(h->order);
   dev_free(h->bmask);
   dev_free(h->ubits);
   dev_free(h->bcv);
@@ -868,7 +1152,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->bcr64);
   h->f[0] = h->f[1] = nullptr;
   h->flags = nullptr;
-  h->rank = h->tiles = h->nbr27 = nullptr;
+  h->rank = h->tiles = h->nbr27 = h->order = nullptr;
   h->bmask = nullptr;
   h->ubits = nullptr;
   h->bcv = h->bcr = nullptr;
@@ -895,6 +1179,16 @@ Halo<T> make_halo(const lbm_handle* h, int q) {
 }
 
 bool halo_on(const lbm_handle* h) { return h->lo.on || h->hi.on; }
+
+// buffer holding the reference's `pre` (AA: the single in-place buffer)
+void* pre_buf(const lbm_handle* h) { return h->g.aa ? h->f[0] : h->f[h->parity]; }
+
+// Geo for readback launches: carries the AA state phase
+Geo rb_geo(const lbm_handle* h) {
+  Geo g = h->g;
+  g.aph = h->g.aa ? h->parity : 0;
+  return g;
+}
 
 long long visits_per_step(const lbm_handle* h) {
   return (h->d.layout == LBM_LAYOUT_DENSE) ? h->n_nodes
@@ -931,13 +1225,29 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
   if (var == 1)
-    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
   else if (var == 2)
-    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
   else
-    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
 }
 
+template <typename T, int TN>
+void launch_tiles_aa(lbm_handle* h, T* F) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
+  const unsigned nt = (unsigned)h->n_tiles;
+  const T* bv = (const T*)h->bcv;
+  const T* br = (const T*)h->bcr;
+  const T om = (T)h->d.omega;
+  constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap
+  if (h->parity == 0)
+    k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+  else
+    k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+}
+
+// one step from `pre` into `post` (AB); AA updates `post` (== pre) in place
 template <typename T>
 int launch_step(lbm_handle* h, const void* pre, void* post) {
   const Geo& g = h->g;
@@ -953,6 +1263,29 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
   constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
+  if (g.aa) {
+    // parity = AA state phase: 0 -> neighbour step, 1 -> node-local step
+    if (!g.tiled) {
+      Planes1<T> F;
+      for (int i = 0; i < Q; ++i) F.f[i] = (T*)post + (size_t)i * g.ps;
+      dim3 grid((g.nxp + 127) / 128, g.ny, g.nz);
+      if (h->parity == 0)
+        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om);
+      else
+        k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om);
+    } else {
+      if (h->n_tiles == 0) return 0;
+      switch (g.tn) {
+        case 32: launch_tiles_aa<T, 32>(h, (T*)post); break;
+        case 64: launch_tiles_aa<T, 64>(h, (T*)post); break;
+        case 128: launch_tiles_aa<T, 128>(h, (T*)post); break;
+        case 256: launch_tiles_aa<T, 256>(h, (T*)post); break;
+        default: launch_tiles_aa<T, 512>(h, (T*)post); break;
+      }
+    }
+    h->launches += 1;
+    return 0;
+  }
   if (!g.tiled) {
     const int bx = 128;
     dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
@@ -1001,10 +1334,11 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
   if (d.dtype != LBM_F32 && d.dtype != LBM_F64) return fail(LBM_EINVAL, "dtype must be LBM_F32 or LBM_F64");
   if (d.layout < 0 || d.layout > LBM_LAYOUT_POINTER_TILE) return fail(LBM_EINVAL, "unknown layout %d", d.layout);
   if (!(d.omega > 0.0 && d.omega < 2.0)) return fail(LBM_EINVAL, "omega must lie in (0, 2), got %g", d.omega);
+  if (d.scheme != LBM_SCHEME_AB && d.scheme != LBM_SCHEME_AA) return fail(LBM_EINVAL, "unknown scheme %d", d.scheme);
   const int nzg = d.nz_global > 0 ? d.nz_global : d.nz;
   if (d.z0 < 0 || d.z0 + d.nz > nzg) return fail(LBM_EINVAL, "slab [%d, %d) outside nz_global %d", d.z0, d.z0 + d.nz, nzg);
-  if (!is_tiled(d.layout) && (long long)(d.nz + 2) * d.ny * ((d.nx + 31) / 32 * 32) >= (1LL << 31))
-    return fail(LBM_EINVAL, "dense slab of %d x %d x %d nodes exceeds 2^31 slots; split it into z-slabs", d.nx, d.ny, d.nz);
+  if (!is_tiled(d.layout) && (long long)(d.nz + 2) * d.ny * ((d.nx + 31) / 32 * 32) + 64 >= (1LL << 32))
+    return fail(LBM_EINVAL, "dense slab of %d x %d x %d nodes exceeds 2^32 slots; split it into z-slabs", d.nx, d.ny, d.nz);
   if (is_tiled(d.layout)) {
     for (int a = 0; a < 3; ++a) {
       const int e = d.tile[a];
@@ -1018,6 +1352,7 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
         return fail(LBM_EINVAL, "periodic axis %d needs extent %d divisible by the tile edge %d", a, n3[a], d.tile[a]);
     if (nzg != d.nz) return fail(LBM_EINVAL, "tile layouts are single-slab in this build");
   }
+  if (d.scheme == LBM_SCHEME_AA && nzg != d.nz) return fail(LBM_EINVAL, "the AA scheme is single-slab in this build");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (d.device < 0 || d.device >= ndev) return fail(LBM_EINVAL, "device %d not present (%d devices)", d.device, ndev);
@@ -1034,6 +1369,7 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
   g.py = d.periodic[1] != 0;
   g.pzw = (d.periodic[2] != 0) && (nzg == d.nz);
   g.tiled = is_tiled(d.layout);
+  g.aa = d.scheme == LBM_SCHEME_AA;
   {
     const char* zf = getenv("LBM_ZERO_FILL");  // A/B switch for the sector-completion stores
     g.zero_fill = (zf && zf[0] == '0') ? 0 : 1;
@@ -1041,6 +1377,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     h->variant = sv ? atoi(sv) : 0;
     const char* ub = getenv("LBM_UBITS");
     h->use_ubits = !(ub && ub[0] == '0');
+    const char* to = getenv("LBM_TILE_ORDER");  // "row": launch tiles in rank order
+    h->morton = to && to[0] == 'm';  // measured: rank order is as fast or faster
     const char* gv = getenv("LBM_GRAPH");
     h->use_graph = !(gv && gv[0] == '0');
   }
@@ -1244,6 +1582,25 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         k_tile_nbr<<<(unsigned)((T * 27 + 255) / 256), 256, 0, h->stream>>>(h->nbr27, h->tiles, h->rank, g, T);
         CKL();
       }
+      if (T > 0 && h->morton) {
+        unsigned long long *k0 = nullptr, *k1 = nullptr;
+        int* v0 = nullptr;
+        void* st = nullptr;
+        size_t sb = 0;
+        if ((rc = dev_alloc(h, &k0, T * 8)) || (rc = dev_alloc(h, &k1, T * 8)) || (rc = dev_alloc(h, &v0, T * 4)) ||
+            (rc = dev_alloc(h, &h->order, T * 4)))
+          goto done;
+        k_tile_morton<<<(unsigned)((T + 255) / 256), 256, 0, h->stream>>>(k0, v0, h->tiles, T);
+        CKL();
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, k0, k1, v0, h->order, (int)T, 0, 63, h->stream));
+        if ((rc = dev_alloc(h, (char**)&st, sb))) goto done;
+        CK(cub::DeviceRadixSort::SortPairs(st, sb, k0, k1, v0, h->order, (int)T, 0, 63, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        dev_free(k0);
+        dev_free(k1);
+        dev_free(v0);
+        dev_free(st);
+      }
       h->n_slots = T * g.tn;
       g.ps = h->n_slots;  // AoSoA: 19 * ps elements = T tiles x 19 blocks
       h->nflags = h->n_slots;
@@ -1269,7 +1626,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         long long live = 0, uni = 0;
         for (size_t k = 0; k < hb.size(); ++k) (k % 8 < 4 ? live : uni) += __builtin_popcount(hb[k]);
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag words
-        h->meta_bytes = T * (27 * 4 + 32) + (live - uni) * bn * 4;
+        h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4;
       }
       h->sm.rank = h->rank;
     }
@@ -1282,11 +1639,19 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     if (herr & 2) { rc = fail(LBM_EINVAL, "velocity/pressure node without a valid bc_index or orientation"); goto done; }
     h->n_nonsolid = (long long)nons;
     h->nb = nb;
+    // release the descriptor temporaries before the PDF buffers claim HBM
+    // (a 2^31-node domain needs every byte: 163 GB AA PDFs + 8.6 GB flags)
+    for (void** p : {(void**)&dtype_, (void**)&dorient, (void**)&dbc, (void**)&dglo, (void**)&dghi,
+                     (void**)&keep, (void**)&scan, (void**)&cub_tmp}) {
+      dev_free(*p);
+      *p = nullptr;
+    }
     // PDF buffers
     const size_t fbytes = (size_t)Q * (size_t)(g.ps > 0 ? g.ps : 64) * h->esize;
-    if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes)) || (rc = dev_alloc(h, (char**)&h->f[1], fbytes))) goto done;
+    if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes))) goto done;
+    if (!g.aa && (rc = dev_alloc(h, (char**)&h->f[1], fbytes))) goto done;  // AA: one buffer
     CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->stream));
-    CK(cudaMemsetAsync(h->f[1], 0, fbytes, h->stream));
+    if (h->f[1]) CK(cudaMemsetAsync(h->f[1], 0, fbytes, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->geometry = true;
     h->parity = 0;
@@ -1306,8 +1671,8 @@ done:
     dev_free(cub_tmp);
     // recompute resident bytes (temporaries released)
     if (h->geometry) {
-      long long b = 2LL * Q * (h->g.ps > 0 ? h->g.ps : 64) * h->esize + h->nflags * 4;
-      if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * 30 * 4;
+      long long b = (h->g.aa ? 1LL : 2LL) * Q * (h->g.ps > 0 ? h->g.ps : 64) * h->esize + h->nflags * 4;
+      if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * (30 + 8 + (h->order ? 1 : 0)) * 4;
       h->device_bytes = b;
     }
   }
@@ -1338,7 +1703,7 @@ int lbm_init_equilibrium(lbm_t* h, const double* rho, const double* ux, const do
   if (!rc) {
     const size_t fbytes = (size_t)Q * g.ps * h->esize;
     cudaMemsetAsync(h->f[0], 0, fbytes, h->stream);
-    cudaMemsetAsync(h->f[1], 0, fbytes, h->stream);
+    if (h->f[1]) cudaMemsetAsync(h->f[1], 0, fbytes, h->stream);
     h->parity = 0;
     const int bx = 128;
     if (h->esize == 4)
@@ -1393,9 +1758,9 @@ int lbm_step_async(lbm_t* h, int64_t n) {
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       for (int k = 0; k < kGraphSteps; ++k) {
         if (h->esize == 4)
-          launch_step<float>(h, h->f[h->parity], h->f[1 - h->parity]);
+          launch_step<float>(h, pre_buf(h), h->g.aa ? h->f[0] : h->f[1 - h->parity]);
         else
-          launch_step<double>(h, h->f[h->parity], h->f[1 - h->parity]);
+          launch_step<double>(h, pre_buf(h), h->g.aa ? h->f[0] : h->f[1 - h->parity]);
         h->parity ^= 1;
       }
       CK(cudaStreamEndCapture(h->stream, &gr));
@@ -1414,8 +1779,8 @@ int lbm_step_async(lbm_t* h, int64_t n) {
     }
   }
   for (int64_t k = 0; k < n; ++k) {
-    const void* pre = h->f[h->parity];
-    void* post = h->f[1 - h->parity];
+    const void* pre = pre_buf(h);
+    void* post = h->g.aa ? h->f[0] : h->f[1 - h->parity];
     if (halo) halo_wait(h);   // neighbours pushed my ghosts and finished reading theirs
     if (h->esize == 4)
       launch_step<float>(h, pre, post);
@@ -1455,26 +1820,44 @@ int lbm_step(lbm_t* h, int64_t n) {
   return lbm_synchronize(h);
 }
 
+// z-planes per readback chunk: device staging bounded by kStageBytes, so
+// readbacks work next to a domain that fills HBM
+constexpr long long kStageBytes = 1LL << 30;
+int chunk_planes(const lbm_handle* h, long long bytes_per_node) {
+  const long long plane = (long long)h->g.nx * h->g.ny * bytes_per_node;
+  long long c = kStageBytes / (plane > 0 ? plane : 1);
+  if (c < 1) c = 1;
+  if (c > h->g.nz) c = h->g.nz;
+  if (c > 65535) c = 65535;  // grid z limit
+  return (int)c;
+}
+
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   DeviceGuard dg(h->d.device);
-  const long long N = h->n_nodes;
+  const Geo g = rb_geo(h);
+  const long long pn = (long long)g.nx * g.ny;
+  const int cz = chunk_planes(h, 4 * 8);
+  const long long C = pn * cz;
   double* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, N * 8 * 4);
+  cudaError_t e = cudaMalloc(&d, C * 8 * 4);
   if (e != cudaSuccess) return fail(LBM_ENOMEM, "macroscopic readback: %s", cudaGetErrorString(e));
-  const int bx = 128;
-  const Geo& g = h->g;
-  double *r = d, *a = d + N, *b = d + 2 * N, *c = d + 3 * N;
-  if (h->esize == 4)
-    k_macro<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->sm, g, r, a, b, c);
-  else
-    k_macro<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->sm, g, r, a, b, c);
-  e = cudaGetLastError();
   double* outs[4] = {rho, ux, uy, uz};
-  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
-    if (outs[k]) e = cudaMemcpyAsync(outs[k], d + k * N, N * 8, cudaMemcpyDeviceToHost, h->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  for (int z0 = 0; z0 < g.nz && e == cudaSuccess; z0 += cz) {
+    const int nzc = g.nz - z0 < cz ? g.nz - z0 : cz;
+    const dim3 grid((g.nx + 127) / 128, g.ny, nzc);
+    if (h->esize == 4)
+      k_macro<float><<<grid, 128, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, g, z0, d, d + C,
+                                                  d + 2 * C, d + 3 * C);
+    else
+      k_macro<double><<<grid, 128, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, z0, d, d + C,
+                                                   d + 2 * C, d + 3 * C);
+    e = cudaGetLastError();
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+      if (outs[k]) e = cudaMemcpyAsync(outs[k] + z0 * pn, d + k * C, nzc * pn * 8, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  }
   cudaFree(d);
   if (e != cudaSuccess) return fail(LBM_ECUDA, "macroscopic: %s", cudaGetErrorString(e));
   return 0;
@@ -1484,15 +1867,15 @@ int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   DeviceGuard dg(h->d.device);
-  const Geo& g = h->g;
+  const Geo g = rb_geo(h);
   const unsigned long long none = ~0ULL;
   const long long V = g.tiled ? h->n_slots : h->n_nodes;
   CK(cudaMemcpyAsync(h->uscratch, &none, 8, cudaMemcpyHostToDevice, h->stream));
   const int bx = 128;
   if (h->esize == 4)
-    k_nonfinite<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->sm, g, V, h->uscratch);
+    k_nonfinite<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, g, V, h->uscratch);
   else
-    k_nonfinite<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->sm, g, V, h->uscratch);
+    k_nonfinite<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, V, h->uscratch);
   CKL();
   unsigned long long best = 0;
   CK(cudaMemcpyAsync(&best, h->uscratch, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -1534,9 +1917,11 @@ int lbm_total_mass(lbm_t* h, double* mass) {
   DeviceGuard dg(h->d.device);
   const int nblk = 1184;  // 8 x 148 SMs; fixed so the reduction order is fixed
   if (h->esize == 4)
-    k_mass_partial<float><<<nblk, 256, 0, h->stream>>>((const float*)h->f[h->parity], h->flags, h->g, h->nflags, h->scratch);
+    k_mass_partial<float><<<nblk, 256, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, h->tiles, rb_geo(h),
+                                                       h->nflags, h->scratch);
   else
-    k_mass_partial<double><<<nblk, 256, 0, h->stream>>>((const double*)h->f[h->parity], h->flags, h->g, h->nflags, h->scratch);
+    k_mass_partial<double><<<nblk, 256, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, h->tiles, rb_geo(h),
+                                                        h->nflags, h->scratch);
   k_mass_final<<<1, 256, 0, h->stream>>>(h->scratch, nblk, h->scratch + nblk);
   CKL();
   CK(cudaMemcpyAsync(mass, h->scratch + nblk, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -1548,32 +1933,43 @@ static int pdf_io(lbm_t* h, int which, void* host, bool get) {
   if (!h || !host) return fail(LBM_EINVAL, "NULL argument");
   if (which != 0 && which != 1) return fail(LBM_EINVAL, "which must be 0 (pre) or 1 (post)");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  if (h->g.aa && which != 0) return fail(LBM_EINVAL, "the AA scheme keeps one buffer: there is no post buffer");
   DeviceGuard dg(h->d.device);
-  const long long bytes = (long long)Q * h->n_nodes * h->esize;
-  void* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, bytes);
+  const Geo g = rb_geo(h);
+  const long long N = h->n_nodes, pn = (long long)g.nx * g.ny;
+  const int es = h->esize;
+  const int cz = chunk_planes(h, (long long)Q * es);
+  const long long C = pn * cz;
+  char* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, C * Q * es);
   if (e != cudaSuccess) return fail(LBM_ENOMEM, "pdf staging: %s", cudaGetErrorString(e));
-  void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
-  const Geo& g = h->g;
-  const int bx = 128;
-  if (get) {
-    if (h->esize == 4)
-      k_get_pdf<float><<<node_grid(g, bx), bx, 0, h->stream>>>((const float*)buf, h->sm, g, (float*)d);
-    else
-      k_get_pdf<double><<<node_grid(g, bx), bx, 0, h->stream>>>((const double*)buf, h->sm, g, (double*)d);
-    e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaMemcpyAsync(host, d, bytes, cudaMemcpyDeviceToHost, h->stream);
-  } else {
-    e = cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, h->stream);
-    if (e == cudaSuccess) {
-      if (h->esize == 4)
-        k_set_pdf<float><<<node_grid(g, bx), bx, 0, h->stream>>>((float*)buf, h->sm, g, (const float*)d);
+  void* buf = which == 0 ? pre_buf(h) : h->f[1 - h->parity];
+  char* hb = (char*)host;
+  // canonical (19, nz, ny, nx): one host block per direction and z chunk
+  for (int z0 = 0; z0 < g.nz && e == cudaSuccess; z0 += cz) {
+    const int nzc = g.nz - z0 < cz ? g.nz - z0 : cz;
+    const long long cn = pn * nzc;
+    const dim3 grid((g.nx + 127) / 128, g.ny, nzc);
+    if (!get) {
+      for (int i = 0; i < Q && e == cudaSuccess; ++i)
+        e = cudaMemcpyAsync(d + i * cn * es, hb + (i * N + z0 * pn) * es, cn * es, cudaMemcpyHostToDevice, h->stream);
+      if (e != cudaSuccess) break;
+      if (es == 4)
+        k_set_pdf<float><<<grid, 128, 0, h->stream>>>((float*)buf, h->flags, h->sm, g, z0, (const float*)d);
       else
-        k_set_pdf<double><<<node_grid(g, bx), bx, 0, h->stream>>>((double*)buf, h->sm, g, (const double*)d);
+        k_set_pdf<double><<<grid, 128, 0, h->stream>>>((double*)buf, h->flags, h->sm, g, z0, (const double*)d);
       e = cudaGetLastError();
+    } else {
+      if (es == 4)
+        k_get_pdf<float><<<grid, 128, 0, h->stream>>>((const float*)buf, h->flags, h->sm, g, z0, (float*)d);
+      else
+        k_get_pdf<double><<<grid, 128, 0, h->stream>>>((const double*)buf, h->flags, h->sm, g, z0, (double*)d);
+      e = cudaGetLastError();
+      for (int i = 0; i < Q && e == cudaSuccess; ++i)
+        e = cudaMemcpyAsync(hb + (i * N + z0 * pn) * es, d + i * cn * es, cn * es, cudaMemcpyDeviceToHost, h->stream);
     }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   }
-  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
   cudaFree(d);
   if (e != cudaSuccess) return fail(LBM_ECUDA, "pdf io: %s", cudaGetErrorString(e));
   return 0;
@@ -1589,9 +1985,42 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
   if (!h || !host) return fail(LBM_EINVAL, "NULL argument");
   if (which != 0 && which != 1) return fail(LBM_EINVAL, "which must be 0 (pre) or 1 (post)");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  if (h->g.aa && which != 0) return fail(LBM_EINVAL, "the AA scheme keeps one buffer: there is no post buffer");
   DeviceGuard dg(h->d.device);
-  void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
   const size_t bytes = (size_t)Q * h->g.ps * h->esize;
+  if (h->g.aa) {
+    // decoded pre buffer in the native slot order, staged on the device
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) return fail(LBM_ENOMEM, "field staging: %s", cudaGetErrorString(e));
+    const Geo g = rb_geo(h);
+    const dim3 grid = node_grid(g, 128);
+    if (get) {
+      e = cudaMemsetAsync(d, 0, bytes, h->stream);
+      if (e == cudaSuccess) {
+        if (h->esize == 4)
+          k_field_aa<float, true><<<grid, 128, 0, h->stream>>>((float*)h->f[0], h->flags, h->sm, g, (float*)d);
+        else
+          k_field_aa<double, true><<<grid, 128, 0, h->stream>>>((double*)h->f[0], h->flags, h->sm, g, (double*)d);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaMemcpyAsync(host, d, bytes, cudaMemcpyDeviceToHost, h->stream);
+    } else {
+      e = cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, h->stream);
+      if (e == cudaSuccess) {
+        if (h->esize == 4)
+          k_field_aa<float, false><<<grid, 128, 0, h->stream>>>((float*)h->f[0], h->flags, h->sm, g, (float*)d);
+        else
+          k_field_aa<double, false><<<grid, 128, 0, h->stream>>>((double*)h->f[0], h->flags, h->sm, g, (double*)d);
+        e = cudaGetLastError();
+      }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(LBM_ECUDA, "field io: %s", cudaGetErrorString(e));
+    return 0;
+  }
+  void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
   if (get)
     CK(cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost));
   else
@@ -1667,6 +2096,7 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->meta_bytes_per_step = h->meta_bytes;
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
+  s->scheme = h->d.scheme;
   return 0;
 }
 
@@ -1721,6 +2151,7 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_export");
   if (h->g.tiled) return fail(LBM_EINVAL, "z-slab halos need a dense layout");
+  if (h->g.aa) return fail(LBM_EINVAL, "z-slab halos need the AB scheme in this build");
   DeviceGuard dg(h->d.device);
   HaloBlob b;
   memset(&b, 0, sizeof(b));

@@ -46,7 +46,7 @@ def max_worker_count():
     return 1 if _worker_cap is None else _worker_cap
 
 
-def _desc(dims, periodic, dtype, layout, tile, device, omega, nz_global=None, z0=0):
+def _desc(dims, periodic, dtype, layout, tile, device, omega, nz_global=None, z0=0, scheme="ab"):
     nx, ny, nz = dims
     d = _lib.LbmDesc()
     d.nx, d.ny, d.nz = int(nx), int(ny), int(nz)
@@ -59,6 +59,9 @@ def _desc(dims, periodic, dtype, layout, tile, device, omega, nz_global=None, z0
     d.layout = _lib.LAYOUT_CODES[layout.value]
     d.device = int(device)
     d.omega = float(omega)
+    if scheme not in _lib.SCHEME_CODES:
+        raise ValueError(f"scheme must be one of {sorted(_lib.SCHEME_CODES)}, got {scheme!r}")
+    d.scheme = _lib.SCHEME_CODES[scheme]
     return d
 
 
@@ -167,8 +170,10 @@ class DeviceField:
 
     @property
     def payload_bytes(self):
-        """Both buffers, 19 planes, one slot per allocated node."""
-        return self.n_slots * Q * 2 * self.dtype.itemsize
+        """All buffers (two for AB, one for AA), 19 planes, one slot per
+        allocated node."""
+        nbuf = 1 if self._sim.scheme == "aa" else 2
+        return self.n_slots * Q * nbuf * self.dtype.itemsize
 
     @property
     def allocated_tiles(self):
@@ -201,6 +206,8 @@ class DeviceField:
 
     @property
     def post(self):
+        if self._sim.scheme == "aa":
+            raise AttributeError("the AA scheme updates one buffer in place: there is no post buffer")
         return self._get(1)
 
     @property
@@ -256,7 +263,7 @@ class Simulation:
     (reference kernel.py:155-311)."""
 
     def __init__(self, geometry, params, layout=LayoutKind.DENSE, scalar=np.float64,
-                 device=0, tile=(8, 8, 8), slab=None):
+                 device=0, tile=(8, 8, 8), slab=None, scheme="ab"):
         self.geometry = geometry
         self.params = params
         self.layout = LayoutKind.parse(layout)
@@ -265,12 +272,16 @@ class Simulation:
             raise ValueError(f"scalar must be float32 or float64, got {scalar}")
         self.device = int(device)
         self.tile = tuple(int(t) for t in tile)
+        # "ab": two buffers swapped every step (the reference's PdfField);
+        # "aa": one buffer updated in place (half the memory, same results)
+        self.scheme = str(scheme).lower()
         desc = geometry.descriptors
         self.slab = slab
         nzg, z0, glo, ghi = (None, 0, None, None) if slab is None else \
             (slab.nz_global, slab.z0, slab.ghost_lo, slab.ghost_hi)
         self._handle = _Handle(_desc(desc.dims, desc.periodic, self.dtype, self.layout,
-                                     self.tile, self.device, params.omega, nz_global=nzg, z0=z0))
+                                     self.tile, self.device, params.omega, nz_global=nzg, z0=z0,
+                                     scheme=self.scheme))
         _upload_geometry(self._handle, desc, geometry.boundary_values, ghost_lo=glo, ghost_hi=ghi)
         self.field = DeviceField(self)
         self.initialized = False
@@ -408,6 +419,16 @@ class Simulation:
         h = self._handle
         _lib.check(h.lib.lbm_get_macroscopic(h.h, *[_lib.ptr(a) for a in out]))
         return tuple(out)
+
+    def density_field(self):
+        """Per-node rho only, float64 (n_z, n_y, n_x) -- a quarter of the
+        macroscopic_fields() readback, for domains near the host-memory limit."""
+        self.field.flush()
+        nx, ny, nz = self.geometry.dims
+        rho = np.empty((nz, ny, nx))
+        h = self._handle
+        _lib.check(h.lib.lbm_get_macroscopic(h.h, _lib.ptr(rho), None, None, None))
+        return rho
 
     def total_mass(self):
         self.field.flush()

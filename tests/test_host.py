@@ -29,7 +29,42 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert {s for s, _, _ in _lib.SIGNATURES} == set(syms)
-    assert lib.lbm_abi_version() == 1
+    assert lib.lbm_abi_version() == _lib.ABI_VERSION == 2
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes mirrors of lbm_desc / lbm_stats have the C layout
+    (sizeof and every offsetof, from a gcc build against include/lbm19.h)."""
+    import ctypes as C
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lines = []
+    for cname, py in (("lbm_desc", _lib.LbmDesc), ("lbm_stats", _lib.LbmStats)):
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src = ("#include <stdio.h>\n#include <stddef.h>\n#include \"lbm19.h\"\nint main(void){\n"
+           + "\n".join(lines) + "\nreturn 0;}\n")
+    (tmp_path / "layout.c").write_text(src)
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(tmp_path / "layout.c"), "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {(a, b): int(c) for a, b, c in (l.split() for l in out if l)}
+    for cname, py in (("lbm_desc", _lib.LbmDesc), ("lbm_stats", _lib.LbmStats)):
+        assert got[(cname, "sizeof")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
+
+
+def test_scheme_argument_validation():
+    from paper_2108_13241_b200.kernel import _desc
+    d = _desc((8, 8, 8), (False,) * 3, np.float32, lb.LayoutKind.DENSE, (8, 8, 8), 0, 1.0, scheme="aa")
+    assert d.scheme == 1
+    with pytest.raises(ValueError):
+        _desc((8, 8, 8), (False,) * 3, np.float32, lb.LayoutKind.DENSE, (8, 8, 8), 0, 1.0, scheme="abc")
 
 
 def test_error_codes_without_device():
