@@ -278,11 +278,17 @@ __device__ __forceinline__ unsigned long long spread3(unsigned v) {
   x = (x | x << 2) & 0x1249249249249249ULL;
   return x;
 }
-__global__ void k_tile_morton(unsigned long long* __restrict__ key, int* __restrict__ val,
-                              const int* __restrict__ tiles, long long T) {
+// mode 1: Morton; mode 2: y-pencils of B tile rows -- (y block, z, y, x) with
+// x fastest, so a tile's z neighbour runs gx*B tiles later instead of gx*gy
+__global__ void k_tile_order_key(unsigned long long* __restrict__ key, int* __restrict__ val,
+                                 const int* __restrict__ tiles, long long T, int mode, int B, Geo g) {
   const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= T) return;
-  key[r] = spread3(tiles[3 * r]) | spread3(tiles[3 * r + 1]) << 1 | spread3(tiles[3 * r + 2]) << 2;
+  const unsigned tx = tiles[3 * r], ty = tiles[3 * r + 1], tz = tiles[3 * r + 2];
+  if (mode == 1)
+    key[r] = spread3(tx) | spread3(ty) << 1 | spread3(tz) << 2;
+  else
+    key[r] = ((((unsigned long long)(ty / B) * g.gz + tz) * B + ty % B) * g.gx) + tx;
   val[r] = (int)r;
 }
 
@@ -933,7 +939,9 @@ __device__ __forceinline__ void stage_nbr(int* srel, const int* __restrict__ nbr
 }
 
 // MODE 0: speculative pull + fix-up over all TN slots; MODE 1: select per
-// link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only.
+// link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only;
+// MODE 3: MODE 1 over live bricks; MODE 4: live bricks, warps whose live
+// nodes all have full masks pull unconditionally, the others select per link.
 template <typename T, int TN, int MODE, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
@@ -945,7 +953,9 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
   stage_nbr<TN>(srel, nbr27, t);
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, MODE == 2);
+  constexpr bool kCompact = MODE >= 2;
+  constexpr bool kSelect = MODE == 1 || MODE == 3;
+  const TileBricks tw(bmask, t, g, TN, kCompact);
   __syncthreads();
 #pragma unroll 1
   for (int k = threadIdx.x; k < tw.work; k += BT) {
@@ -954,6 +964,8 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
     const uint32_t w = tw.flag(flags, t, TN, l, in);
     const bool live = flag_type(w) != SOLID;
     const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+    const uint32_t miss = ~w & kMaskBits;
+    const bool fast = MODE == 4 ? __all_sync(0xffffffffu, !live || miss == 0u) : !kSelect;
     if (!live) {
       if (zfill && in) {
 #pragma unroll
@@ -961,11 +973,10 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
       }
       continue;
     }
-    const uint32_t miss = ~w & kMaskBits;
     const TileUp up(g, l);
     T f[Q];
     f[0] = __ldg(tb + l);
-    if (MODE != 1) {
+    if (fast) {
 #pragma unroll
       for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + up.at(srel, i));
       if (miss) {
@@ -1049,7 +1060,8 @@ struct lbm_handle {
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
   int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
-  bool morton = false;
+  int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows
+  int pencil = 4;
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
   uint32_t* ubits = nullptr;  // dense: uniform-chunk bitmap (1 bit per 32 nodes)
   bool use_ubits = true;
@@ -1224,7 +1236,11 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
-  if (var == 1)
+  if (var == 3)
+    k_step_tiles<T, TN, 3, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+  else if (var == 4)
+    k_step_tiles<T, TN, 4, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+  else if (var == 1)
     k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
   else if (var == 2)
     k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
@@ -1378,7 +1394,9 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     const char* ub = getenv("LBM_UBITS");
     h->use_ubits = !(ub && ub[0] == '0');
     const char* to = getenv("LBM_TILE_ORDER");  // "row": launch tiles in rank order
-    h->morton = to && to[0] == 'm';  // measured: rank order is as fast or faster
+    // "morton" | "pencil[:B]" | "row" (rank order)
+    h->order_mode = !to ? 0 : to[0] == 'm' ? 1 : to[0] == 'p' ? 2 : 0;
+    if (to && to[0] == 'p' && strchr(to, ':')) h->pencil = atoi(strchr(to, ':') + 1) > 0 ? atoi(strchr(to, ':') + 1) : 4;
     const char* gv = getenv("LBM_GRAPH");
     h->use_graph = !(gv && gv[0] == '0');
   }
@@ -1582,7 +1600,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         k_tile_nbr<<<(unsigned)((T * 27 + 255) / 256), 256, 0, h->stream>>>(h->nbr27, h->tiles, h->rank, g, T);
         CKL();
       }
-      if (T > 0 && h->morton) {
+      if (T > 0 && h->order_mode) {
         unsigned long long *k0 = nullptr, *k1 = nullptr;
         int* v0 = nullptr;
         void* st = nullptr;
@@ -1590,7 +1608,8 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         if ((rc = dev_alloc(h, &k0, T * 8)) || (rc = dev_alloc(h, &k1, T * 8)) || (rc = dev_alloc(h, &v0, T * 4)) ||
             (rc = dev_alloc(h, &h->order, T * 4)))
           goto done;
-        k_tile_morton<<<(unsigned)((T + 255) / 256), 256, 0, h->stream>>>(k0, v0, h->tiles, T);
+        k_tile_order_key<<<(unsigned)((T + 255) / 256), 256, 0, h->stream>>>(k0, v0, h->tiles, T, h->order_mode,
+                                                                             h->pencil, g);
         CKL();
         CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, k0, k1, v0, h->order, (int)T, 0, 63, h->stream));
         if ((rc = dev_alloc(h, (char**)&st, sb))) goto done;
