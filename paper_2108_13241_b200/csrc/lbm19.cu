@@ -938,19 +938,104 @@ __device__ __forceinline__ void stage_nbr(int* srel, const int* __restrict__ nbr
   }
 }
 
+// z-slab halo for tile layouts: ghost planes (5 populations x ny x nx, row
+// pitch nx) per buffer.  pre_lo / pre_hi: this slab's ghosts of the pre
+// buffer (filled by the neighbours' previous step); push_lo / push_hi: the
+// neighbours' ghosts of the post buffer (peer memory), which this step fills
+// with the c_z = -1 / +1 populations of its bottom / top plane.
+template <typename T>
+struct TileHalo {
+  int on;
+  const int* tiles;
+  const T* pre_lo;   // kZp(j) populations of plane z = -1
+  const T* pre_hi;   // kZm(j) populations of plane z = nz
+  T* push_lo[5];     // lower neighbour's hi ghost (kZm)
+  T* push_hi[5];     // upper neighbour's lo ghost (kZp)
+};
+
+template <typename T>
+__device__ __forceinline__ long long ghost_row(const Geo& g, int x, int y) {
+  if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;  // present links wrap only on periodic axes
+  if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
+  return (long long)y * g.nx + x;
+}
+
+// links into the ghost planes replace the (meaningless) speculative values
+template <typename T>
+__device__ __forceinline__ void tile_ghost_gather(T (&f)[Q], uint32_t miss, const TileHalo<T>& TH, const Geo& g,
+                                                  int x, int y, int z) {
+  const long long pn = (long long)g.nx * g.ny;
+  if (z == 0 && TH.pre_lo) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZp(j);
+      if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = __ldg(TH.pre_lo + j * pn + ghost_row<T>(g, x - cx(i), y - cy(i)));
+    }
+  }
+  if (z == g.nz - 1 && TH.pre_hi) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZm(j);
+      if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = __ldg(TH.pre_hi + j * pn + ghost_row<T>(g, x - cx(i), y - cy(i)));
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_ghost_push(const T (&f)[Q], const TileHalo<T>& TH, const Geo& g, int x, int y,
+                                                int z) {
+  const long long r = (long long)y * g.nx + x;
+  if (z == 0 && TH.push_lo[0]) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) TH.push_lo[j][r] = f[kZm(j)];
+    __threadfence_system();
+  }
+  if (z == g.nz - 1 && TH.push_hi[0]) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) TH.push_hi[j][r] = f[kZp(j)];
+    __threadfence_system();
+  }
+}
+
+// initial ghost fill for tile layouts: boundary planes of `pre`
+template <typename T>
+__global__ void k_tile_halo_push(const T* __restrict__ pre, SlotMap sm, Geo g, TileHalo<T> TH) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (x >= g.nx) return;
+  const long long r = (long long)y * g.nx + x;
+  const long long s0 = sm.slot(g, x, y, 0), s1 = sm.slot(g, x, y, g.nz - 1);
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (TH.push_lo[0]) TH.push_lo[j][r] = s0 >= 0 ? pre[fidx(g, kZm(j), s0)] : (T)0;
+    if (TH.push_hi[0]) TH.push_hi[j][r] = s1 >= 0 ? pre[fidx(g, kZp(j), s1)] : (T)0;
+  }
+  __threadfence_system();
+}
+
 // MODE 0: speculative pull + fix-up over all TN slots; MODE 1: select per
 // link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only;
 // MODE 3: MODE 1 over live bricks; MODE 4: live bricks, warps whose live
 // nodes all have full masks pull unconditionally, the others select per link.
-template <typename T, int TN, int MODE, int MINB>
+template <typename T, int TN, int MODE, int MINB, bool CUT = false>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
              const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-             const uint32_t* __restrict__ bmask, const int* __restrict__ order) {
+             const uint32_t* __restrict__ bmask, const int* __restrict__ order, const TileHalo<T> TH) {
   constexpr int BT = TN < 256 ? TN : 256;
   __shared__ int srel[27];
   const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
   stage_nbr<TN>(srel, nbr27, t);
+  // z-slab cut: tiles on the first / last tile plane exchange their boundary
+  // nodes' c_z populations through ghost planes (uniform per CTA)
+  int tz0 = 0, tx0 = 0, ty0 = 0;
+  bool cut = false;
+  if (CUT) {
+    tx0 = __ldg(TH.tiles + 3 * t) * g.ex;
+    ty0 = __ldg(TH.tiles + 3 * t + 1) * g.ey;
+    tz0 = __ldg(TH.tiles + 3 * t + 2) * g.ez;
+    cut = tz0 == 0 || tz0 + g.ez >= g.nz;
+  }
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
   constexpr bool kCompact = MODE >= 2;
@@ -989,9 +1074,18 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
       for (int i = 1; i < Q; ++i)
         f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : i * TN + up.at(srel, i)));
     }
+    int x = 0, y = 0, z = -1;
+    if (CUT && cut) {
+      brick_inv(g, l, x, y, z);
+      x += tx0;
+      y += ty0;
+      z += tz0;
+      tile_ghost_gather<T>(f, miss, TH, g, x, y, z);
+    }
     bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
     for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+    if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
   }
 }
 
@@ -1060,6 +1154,8 @@ struct lbm_handle {
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
   int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
+  void* gh[2] = {nullptr, nullptr};  // tile slabs: ghost planes per buffer, [lo | hi] x 5 x ny x nx
+  bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
   int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows
   int pencil = 4;
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
@@ -1155,6 +1251,9 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->tiles);
   dev_free(h->nbr27);
   dev_free(h->order);
+  dev_free(h->gh[0]);
+  dev_free(h->gh[1]);
+  h->gh[0] = h->gh[1] = nullptr;
   dev_free(h->bmask);
   dev_free(h->ubits);
   dev_free(h->bcv);
@@ -1190,6 +1289,22 @@ Halo<T> make_halo(const lbm_handle* h, int q) {
   return H;
 }
 
+template <typename T>
+TileHalo<T> make_tile_halo(const lbm_handle* h, int q_pre, int q_post) {
+  TileHalo<T> TH{};
+  TH.on = h->g.tiled && h->gh[0] != nullptr;
+  if (!TH.on) return TH;
+  const size_t pn = (size_t)h->g.nx * h->g.ny;
+  TH.tiles = h->tiles;
+  TH.pre_lo = h->has_glo ? (const T*)h->gh[q_pre] : nullptr;
+  TH.pre_hi = h->has_ghi ? (const T*)h->gh[q_pre] + 5 * pn : nullptr;
+  for (int j = 0; j < 5; ++j) {
+    TH.push_lo[j] = h->lo.on ? (T*)h->lo.f[q_post] + (5 + j) * pn : nullptr;
+    TH.push_hi[j] = h->hi.on ? (T*)h->hi.f[q_post] + j * pn : nullptr;
+  }
+  return TH;
+}
+
 bool halo_on(const lbm_handle* h) { return h->lo.on || h->hi.on; }
 
 // buffer holding the reference's `pre` (AA: the single in-place buffer)
@@ -1222,6 +1337,13 @@ void halo_wait(lbm_handle* h) {
 
 template <typename T>
 void halo_push(lbm_handle* h) {
+  if (h->g.tiled) {
+    const TileHalo<T> TH = make_tile_halo<T>(h, h->parity, h->parity);
+    h->launches += 1;
+    k_tile_halo_push<T><<<dim3((h->g.nx + 127) / 128, h->g.ny), 128, 0, h->stream>>>((const T*)h->f[h->parity], h->sm,
+                                                                                     h->g, TH);
+    return;
+  }
   const Halo<T> H = make_halo<T>(h, h->parity);
   h->launches += 1;
   dim3 grid((h->g.nxp + 127) / 128, h->g.ny);
@@ -1231,21 +1353,28 @@ void halo_push(lbm_handle* h) {
 template <typename T, int TN>
 void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   constexpr int BT = TN < 256 ? TN : 256;
+  const TileHalo<T> TH = make_tile_halo<T>(h, h->parity, 1 - h->parity);
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
   const unsigned nt = (unsigned)h->n_tiles;
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
+  if (TH.on) {  // z-slab: the live-brick kernel with the ghost-plane exchange
+    k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
+        pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                               h->bmask, h->order, TH);
+    return;
+  }
   if (var == 3)
-    k_step_tiles<T, TN, 3, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles<T, TN, 3, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 4)
-    k_step_tiles<T, TN, 4, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles<T, TN, 4, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 1)
-    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 2)
-    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else
-    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
 }
 
 template <typename T, int TN>
@@ -1328,6 +1457,42 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
   return 0;
 }
 
+// CUDA lazy module loading loads a kernel at its first launch, and loading
+// waits for the device: with a neighbour's k_halo_wait spinning, that first
+// launch would stall until the wait times out.  A slab therefore loads every
+// kernel its step loop can launch when it is connected, before any spins.
+template <typename T, int TN>
+void preload_tiles(cudaFuncAttributes* a) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
+  cudaFuncGetAttributes(a, k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true>);
+}
+
+template <typename T>
+void preload_halo_kernels(const lbm_handle* h) {
+  constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_halo_wait);
+  cudaFuncGetAttributes(&a, k_halo_signal);
+  if (!h->g.tiled) {
+    cudaFuncGetAttributes(&a, k_halo_push<T>);
+    cudaFuncGetAttributes(&a, k_step_dense<T, 0, D1>);
+    cudaFuncGetAttributes(&a, k_step_dense<T, 1, D1>);
+    cudaFuncGetAttributes(&a, k_step_dense<T, 0, D2>);
+    cudaFuncGetAttributes(&a, k_step_dense<T, 1, D2>);
+  } else {
+    cudaFuncGetAttributes(&a, k_tile_halo_push<T>);
+    switch (h->g.tn) {
+      case 32: preload_tiles<T, 32>(&a); break;
+      case 64: preload_tiles<T, 64>(&a); break;
+      case 128: preload_tiles<T, 128>(&a); break;
+      case 256: preload_tiles<T, 256>(&a); break;
+      default: preload_tiles<T, 512>(&a); break;
+    }
+  }
+  cudaGetLastError();
+}
+
 }  // namespace
 
 // ================================================================= C-ABI
@@ -1366,7 +1531,6 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     for (int a = 0; a < 3; ++a)
       if (d.periodic[a] && n3[a] % d.tile[a])
         return fail(LBM_EINVAL, "periodic axis %d needs extent %d divisible by the tile edge %d", a, n3[a], d.tile[a]);
-    if (nzg != d.nz) return fail(LBM_EINVAL, "tile layouts are single-slab in this build");
   }
   if (d.scheme == LBM_SCHEME_AA && nzg != d.nz) return fail(LBM_EINVAL, "the AA scheme is single-slab in this build");
   int ndev = 0;
@@ -1648,6 +1812,15 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4;
       }
       h->sm.rank = h->rank;
+      // z-slab ghost planes (tile layouts keep them outside the tile storage)
+      h->has_glo = ghost_lo != nullptr;
+      h->has_ghi = ghost_hi != nullptr;
+      if (h->has_glo || h->has_ghi) {
+        const size_t gb = (size_t)10 * plane_nodes * h->esize;
+        if ((rc = dev_alloc(h, (char**)&h->gh[0], gb)) || (rc = dev_alloc(h, (char**)&h->gh[1], gb))) goto done;
+        CK(cudaMemsetAsync(h->gh[0], 0, gb, h->stream));
+        CK(cudaMemsetAsync(h->gh[1], 0, gb, h->stream));
+      }
     }
     int herr = 0;
     unsigned long long nons = 0;
@@ -1692,6 +1865,7 @@ done:
     if (h->geometry) {
       long long b = (h->g.aa ? 1LL : 2LL) * Q * (h->g.ps > 0 ? h->g.ps : 64) * h->esize + h->nflags * 4;
       if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * (30 + 8 + (h->order ? 1 : 0)) * 4;
+      if (h->gh[0]) b += 2LL * 10 * h->g.nx * h->g.ny * h->esize;
       h->device_bytes = b;
     }
   }
@@ -2123,7 +2297,7 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
 namespace {
 struct HaloBlob {
   uint32_t magic;
-  int32_t device, esize, nz, ny, nxp;
+  int32_t device, esize, nz, ny, nxp, tiled;
   int64_t pid, ps;
   void* f[2];
   void* sync;
@@ -2135,8 +2309,8 @@ static_assert(sizeof(HaloBlob) <= LBM_HALO_BLOB_BYTES, "halo blob too large");
 
 int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
   if (b.magic != kHaloMagic) return fail(LBM_EINVAL, "not a halo blob");
-  if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp)
-    return fail(LBM_EINVAL, "neighbouring slab has a different dtype or x/y extent");
+  if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp || b.tiled != h->g.tiled)
+    return fail(LBM_EINVAL, "neighbouring slab has a different dtype, layout family or x/y extent");
   if (b.pid == (int64_t)getpid()) {
     if (b.device != h->d.device) {
       int can = 0;
@@ -2169,8 +2343,8 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
 int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_export");
-  if (h->g.tiled) return fail(LBM_EINVAL, "z-slab halos need a dense layout");
   if (h->g.aa) return fail(LBM_EINVAL, "z-slab halos need the AB scheme in this build");
+  if (h->g.tiled && !h->gh[0]) return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
   DeviceGuard dg(h->d.device);
   HaloBlob b;
   memset(&b, 0, sizeof(b));
@@ -2182,11 +2356,14 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   b.nxp = h->g.nxp;
   b.pid = (int64_t)getpid();
   b.ps = h->g.ps;
-  b.f[0] = h->f[0];
-  b.f[1] = h->f[1];
+  b.tiled = h->g.tiled;
+  // dense: the PDF buffers (ghost planes inside); tiles: the ghost-plane buffers
+  void* const* ex = h->g.tiled ? h->gh : h->f;
+  b.f[0] = ex[0];
+  b.f[1] = ex[1];
   b.sync = h->sync;
-  CK(cudaIpcGetMemHandle(&b.ipc_f[0], h->f[0]));
-  CK(cudaIpcGetMemHandle(&b.ipc_f[1], h->f[1]));
+  CK(cudaIpcGetMemHandle(&b.ipc_f[0], ex[0]));
+  CK(cudaIpcGetMemHandle(&b.ipc_f[1], ex[1]));
   CK(cudaIpcGetMemHandle(&b.ipc_sync, h->sync));
   memset(blob, 0, LBM_HALO_BLOB_BYTES);
   memcpy(blob, &b, sizeof(b));
@@ -2197,7 +2374,8 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
 int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_connect");
-  if (h->g.tiled) return fail(LBM_EINVAL, "z-slab halos need a dense layout");
+  if (h->g.tiled && !h->gh[0] && (lo_blob || hi_blob))
+    return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
   if (h->g.pzw && (lo_blob || hi_blob))
     return fail(LBM_EINVAL, "a whole-domain periodic handle wraps z itself; it takes no halo");
   DeviceGuard dg(h->d.device);
@@ -2212,6 +2390,7 @@ int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
     memcpy(&b, hi_blob, sizeof(b));
     if ((rc = open_peer(h, b, h->hi))) return rc;
   }
+  if (h->esize == 4) preload_halo_kernels<float>(h); else preload_halo_kernels<double>(h);
   h->halo_dirty = true;
   return 0;
 }

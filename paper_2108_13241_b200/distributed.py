@@ -38,6 +38,29 @@ def split_z(nz, parts):
     return out
 
 
+def split_z_balanced(type_tag, parts, align=1):
+    """Contiguous z ranges [(z0, z1), ...] with cuts on multiples of `align`
+    (the tile edge for tile layouts, so every slab starts on a tile plane)
+    that balance the non-solid node count -- the unit of work of a sparse
+    step.  Each slab keeps at least one aligned block."""
+    nz = type_tag.shape[0]
+    nblk = -(-nz // align)
+    if parts < 1 or parts > nblk:
+        raise ValueError(f"cannot split {nz} planes into {parts} slabs aligned to {align}")
+    per_plane = np.count_nonzero(type_tag.reshape(nz, -1), axis=1)
+    per_blk = np.add.reduceat(per_plane, np.arange(0, nz, align))
+    cum = np.concatenate([[0], np.cumsum(per_blk)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, parts):
+        # block boundary closest to the r-th share, leaving room for the rest
+        b = int(np.argmin(np.abs(cum - total * r / parts)))
+        b = min(max(b, cuts[-1] + 1), nblk - (parts - r))
+        cuts.append(b)
+    cuts.append(nblk)
+    return [(c0 * align, min(c1 * align, nz)) for c0, c1 in zip(cuts[:-1], cuts[1:])]
+
+
 def neighbours(rank, world, periodic_z):
     lo = rank - 1 if rank > 0 else (world - 1 if periodic_z and world > 1 else None)
     hi = rank + 1 if rank < world - 1 else (0 if periodic_z and world > 1 else None)

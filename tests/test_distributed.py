@@ -111,3 +111,27 @@ def test_channel_and_duct_slab_builders_match_global():
     fc = lb.build_channel(16, 12, 12, lb.VelocityInlet((0.05, 0.0, 0.0)))
     assert np.array_equal(c.descriptors.type_tag, fc.descriptors.type_tag[8:12])
     assert cs.nz_global == 12 and cs.z0 == 8
+
+
+def test_split_z_balanced_tile_aligned():
+    from paper_2108_13241_b200.distributed import split_z_balanced
+    rng = np.random.default_rng(0)
+    types = np.zeros((64, 8, 8), dtype=np.uint8)
+    # non-solid mass concentrated at the top: equal plane counts would be unbalanced
+    for z in range(64):
+        types[z].flat[: int(64 * (z / 63) ** 2)] = 1
+    for parts, align in ((2, 8), (4, 8), (3, 4), (8, 8), (5, 1)):
+        cuts = split_z_balanced(types, parts, align)
+        assert cuts[0][0] == 0 and cuts[-1][1] == 64 and len(cuts) == parts
+        assert all(a % align == 0 and b > a for a, b in cuts)
+        assert all(cuts[k][1] == cuts[k + 1][0] for k in range(parts - 1))
+        loads = [int(np.count_nonzero(types[a:b])) for a, b in cuts]
+        # within one aligned block of the ideal share
+        blk = max(int(np.count_nonzero(types[z:z + align])) for z in range(0, 64, align))
+        assert max(loads) - min(loads) <= 2 * blk
+    with pytest.raises(ValueError):
+        split_z_balanced(types, 9, 8)
+    ragged = rng.integers(0, 2, size=(30, 4, 4)).astype(np.uint8)
+    cuts = split_z_balanced(ragged, 3, 8)
+    assert cuts[-1] == (16, 30) or cuts[-1][1] == 30
+

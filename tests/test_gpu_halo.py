@@ -10,7 +10,8 @@ import pytest
 
 import paper_2108_13241_b200 as lb
 from helpers import oracle_sim, random_mixed_geometry3, to_geometry
-from paper_2108_13241_b200.distributed import connect_local, slab_geometry, split_z
+from paper_2108_13241_b200.distributed import (connect_local, slab_geometry, split_z,
+                                                split_z_balanced)
 
 pytestmark = pytest.mark.gpu
 
@@ -52,13 +53,50 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     assert np.array_equal(single.canonical_state(), ref.pre)
 
 
+@pytest.mark.parametrize("layout,tile,nslab,periodic_z,dtype", [
+    ("pointer_tile", (8, 4, 4), 2, False, np.float32),
+    ("pointer_tile", (8, 4, 4), 3, True, np.float64),
+    ("pointer_tile", (4, 4, 2), 5, True, np.float32),
+    ("tile", (8, 8, 4), 2, True, np.float32),
+    ("pointer_tile", (8, 8, 8), 2, False, np.float64)])
+def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
+    """Sparse z-slabs: cuts on tile planes balanced by non-solid count; the
+    boundary tiles exchange through ghost planes inside the step kernel."""
+    c = random_mixed_geometry3(13, n=(19, 12, 24), periodic_z=periodic_z)
+    geom = to_geometry(c)
+    params = _params(1.25)
+    single = lb.Simulation(geom, params, layout=layout, scalar=dtype, tile=tile)
+    single.initialize(1.0)
+    sims = []
+    cuts = split_z_balanced(geom.descriptors.type_tag, nslab, align=tile[2])
+    for z0, z1 in cuts:
+        assert z0 % tile[2] == 0
+        g, spec = slab_geometry(geom, z0, z1)
+        sims.append(lb.Simulation(g, params, layout=layout, scalar=dtype, tile=tile, slab=spec))
+    connect_local(sims, periodic_z)
+    for s in sims:
+        s.initialize(1.0)
+    for chunk in (1, 2, 13):
+        single.step(chunk)
+        for s in sims:
+            s.step(chunk, block=False)
+        for s in sims:
+            s.synchronize()
+        got = np.concatenate([s.canonical_state() for s in sims], axis=1)
+        assert np.array_equal(got, single.canonical_state()), chunk
+    ref = oracle_sim(c, params.omega, dtype)
+    ref.initialize(1.0)
+    ref.step(16)
+    assert np.array_equal(single.canonical_state(), ref.pre)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _ipc_worker(rank, world, port, out_dir):
+def _ipc_worker(rank, world, port, out_dir, layout="dense"):
     import torch.distributed as dist
     from paper_2108_13241_b200.distributed import connect_distributed
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -68,7 +106,8 @@ def _ipc_worker(rank, world, port, out_dir):
     geom = to_geometry(c)
     z0, z1 = split_z(14, world)[rank]
     g, spec = slab_geometry(geom, z0, z1)
-    sim = lb.Simulation(g, _params(1.1), scalar=np.float32, slab=spec, device=0)
+    sim = lb.Simulation(g, _params(1.1), layout=layout, scalar=np.float32, slab=spec, device=0,
+                        tile=(8, 4, 1))
     connect_distributed(sim, periodic_z=True)
     sim.initialize(1.0)
     sim.step(25)
@@ -78,9 +117,10 @@ def _ipc_worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_slabs_two_processes_ipc_bitwise(tmp_path):
+@pytest.mark.parametrize("layout", ["dense", "pointer_tile"])
+def test_slabs_two_processes_ipc_bitwise(tmp_path, layout):
     import torch.multiprocessing as mp
-    mp.spawn(_ipc_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_ipc_worker, args=(2, _free_port(), str(tmp_path), layout), nprocs=2, join=True)
     c = random_mixed_geometry3(12, n=(21, 10, 14), periodic_z=True)
     single = lb.Simulation(to_geometry(c), _params(1.1), scalar=np.float32)
     single.initialize(1.0)
