@@ -242,6 +242,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
+    ap.add_argument("--tile", default="8,8,8", help="tile edges x,y,z for tile layouts")
     ap.add_argument("--scheme", default=None, choices=["ab", "aa"],
                     help="PDF storage: two buffers (ab) or one in place (aa)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -267,6 +268,7 @@ def main():
     workload = args.workload or "channel512"
     geom, params, layout, desc, rho0 = build_workload(workload)
     scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
+    tile = tuple(int(v) for v in args.tile.split(","))
     if args.variants:
         for v in args.variants.split(","):
             # "3" selects LBM_STEP_VARIANT=3; "KEY=VAL;KEY=VAL" sets library switches
@@ -277,7 +279,7 @@ def main():
             else:
                 os.environ["LBM_STEP_VARIANT"] = v
             sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
-                                scheme=scheme)
+                                scheme=scheme, tile=tile)
             sim.initialize(rho0)
             sim.step(args.warmup)
             sim.step(args.steps)
@@ -287,12 +289,13 @@ def main():
             peak, _ = measured_peak()
             alg = nons * PDF_BYTES_PER_NODE_F32 + int(sim.stats().meta_bytes_per_step)
             frac = alg / (ms / args.steps / 1e3) / 1e9 / peak
-            print(json.dumps({"workload": workload, "variant": v, "mlups": round(mlups),
+            print(json.dumps({"workload": workload, "variant": v, "tile": args.tile, "mlups": round(mlups),
                               "frac": round(frac, 4), "alg_B_per_node": round(alg / nons, 2),
                               "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
         return
-    sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local, scheme=scheme)
+    sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local, scheme=scheme,
+                        tile=tile)
     sim.initialize(rho0)
     sim.step(args.warmup)
     launches0 = sim.launches_total
@@ -326,7 +329,7 @@ def main():
         d2h = (1 if big else 4) * 8 * nx * ny * nz
         t0 = time.perf_counter()
         s2 = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
-                           scheme=scheme)
+                           scheme=scheme, tile=tile)
         s2.initialize(rho0)
         s2.step(args.steps)
         fields = s2.density_field() if big else s2.macroscopic_fields()
@@ -350,7 +353,9 @@ def main():
         "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "layout": layout, "scheme": scheme, "nodes": int(st.n_nodes),
+        "config": {"workload": desc, "layout": layout, "scheme": scheme,
+                   "tile": list(tile) if layout in ("tile", "pointer_tile") else None,
+                   "nodes": int(st.n_nodes),
                    "non_solid_nodes": int(nons), "tiles": int(st.n_tiles),
                    "l2": "state 2x19 planes >> 126 MB L2 (no flush needed)",
                    "parallelism": "single GPU"},
