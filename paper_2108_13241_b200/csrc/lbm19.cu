@@ -32,6 +32,7 @@
 #include <cstring>
 #include <unistd.h>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "d3q19.cuh"
@@ -1176,6 +1177,9 @@ struct lbm_handle {
   double last_ms = 0.0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* pin[2] = {nullptr, nullptr};   // pinned host staging for pipelined readbacks
+  size_t pin_bytes = 0;
+  cudaEvent_t evc[2] = {nullptr, nullptr};
   double* scratch = nullptr;   // reductions
   unsigned long long* uscratch = nullptr;
   // z-slab halo (fused peer stores); see k_step_dense and lbm_halo_connect
@@ -1365,10 +1369,12 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
                                                                h->bmask, h->order, TH);
     return;
   }
+  // the select variants need more registers than the speculative gather
+  constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;
   if (var == 3)
-    k_step_tiles<T, TN, 3, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
+    k_step_tiles<T, TN, 3, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 4)
-    k_step_tiles<T, TN, 4, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
+    k_step_tiles<T, TN, 4, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 1)
     k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 2)
@@ -1638,6 +1644,10 @@ void lbm_destroy(lbm_t* h) {
   dev_free(h->uscratch);
   dev_free(h->sync);
   dev_free(h->herr);
+  for (int b = 0; b < 2; ++b) {
+    if (h->pin[b]) cudaFreeHost(h->pin[b]);
+    if (h->evc[b]) cudaEventDestroy(h->evc[b]);
+  }
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -2025,35 +2035,122 @@ int chunk_planes(const lbm_handle* h, long long bytes_per_node) {
   return (int)c;
 }
 
+extern "C++" {
+// host copy split over threads (also spreads the page faults of fresh
+// destination arrays)
+static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
+  size_t total = 0;
+  for (size_t v : n) total += v;
+  const int nt = total > (8u << 20) ? 8 : 1;
+  auto work = [&](int t) {
+    for (size_t k = 0; k < n.size(); ++k) {
+      const size_t per = (n[k] + nt - 1) / nt, a = per * t, b = a + per < n[k] ? a + per : n[k];
+      if (a < b) memcpy(dst_src[k].first + a, dst_src[k].second + a, b - a);
+    }
+  };
+  if (nt == 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
+// Pipelined device -> host readback in z chunks: chunk k's kernel and D2H
+// copy (into pinned staging) overlap the host copy of chunk k-1 out of the
+// other pinned slot.  launch(k, z0, nzc, dev) enqueues the chunk kernel;
+// consume(k, z0, nzc, pinned) copies it into the caller's arrays.
+template <class Launch, class Consume>
+static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch, Consume consume) {
+  const long long pn = (long long)h->g.nx * h->g.ny;
+  const size_t want = 64u << 20;  // per staging slot
+  long long cz = (long long)want / (pn * bytes_per_node);
+  if (cz < 1) cz = 1;
+  if (cz > h->g.nz) cz = h->g.nz;
+  if (cz > 65535) cz = 65535;
+  const size_t slot = (size_t)(cz * pn * bytes_per_node);
+  if (h->pin_bytes < slot) {
+    for (int b = 0; b < 2; ++b) {
+      if (h->pin[b]) cudaFreeHost(h->pin[b]);
+      h->pin[b] = nullptr;
+    }
+    h->pin_bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
+      }
+    h->pin_bytes = slot;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
+  char* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, 2 * slot);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "readback staging: %s", cudaGetErrorString(e));
+  const int nz = h->g.nz;
+  const int nchunk = (int)((nz + cz - 1) / cz);
+  for (int k = 0; k <= nchunk && e == cudaSuccess; ++k) {
+    if (k < nchunk) {
+      const int b = k & 1, z0 = (int)(k * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
+      launch(k, z0, nzc, dev + b * slot);
+      e = cudaGetLastError();
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->pin[b], dev + b * slot, (size_t)(nzc * pn * bytes_per_node), cudaMemcpyDeviceToHost,
+                            h->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->evc[b], h->stream);
+    }
+    if (k > 0 && e == cudaSuccess) {
+      const int b = (k - 1) & 1, z0 = (int)((k - 1) * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
+      e = cudaEventSynchronize(h->evc[b]);
+      if (e == cudaSuccess) consume(k - 1, z0, nzc, (const char*)h->pin[b]);
+    }
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(dev);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "readback: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+}  // extern "C++"
+
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   DeviceGuard dg(h->d.device);
   const Geo g = rb_geo(h);
   const long long pn = (long long)g.nx * g.ny;
-  const int cz = chunk_planes(h, 4 * 8);
-  const long long C = pn * cz;
-  double* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, C * 8 * 4);
-  if (e != cudaSuccess) return fail(LBM_ENOMEM, "macroscopic readback: %s", cudaGetErrorString(e));
   double* outs[4] = {rho, ux, uy, uz};
-  for (int z0 = 0; z0 < g.nz && e == cudaSuccess; z0 += cz) {
-    const int nzc = g.nz - z0 < cz ? g.nz - z0 : cz;
+  int nf = 0, which[4];
+  for (int k = 0; k < 4; ++k)
+    if (outs[k]) which[nf++] = k;
+  if (!nf) return 0;
+  // staging chunk: the requested fields back to back, (nf, nzc * pn) doubles
+  auto launch = [&](int, int z0, int nzc, char* dev) {
+    double* d = (double*)dev;
+    const long long C = (long long)nzc * pn;
+    double* f[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int j = 0; j < nf; ++j) f[which[j]] = d + j * C;
     const dim3 grid((g.nx + 127) / 128, g.ny, nzc);
     if (h->esize == 4)
-      k_macro<float><<<grid, 128, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, g, z0, d, d + C,
-                                                  d + 2 * C, d + 3 * C);
+      k_macro<float><<<grid, 128, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, g, z0, f[0], f[1], f[2],
+                                                  f[3]);
     else
-      k_macro<double><<<grid, 128, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, z0, d, d + C,
-                                                   d + 2 * C, d + 3 * C);
-    e = cudaGetLastError();
-    for (int k = 0; k < 4 && e == cudaSuccess; ++k)
-      if (outs[k]) e = cudaMemcpyAsync(outs[k] + z0 * pn, d + k * C, nzc * pn * 8, cudaMemcpyDeviceToHost, h->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-  }
-  cudaFree(d);
-  if (e != cudaSuccess) return fail(LBM_ECUDA, "macroscopic: %s", cudaGetErrorString(e));
-  return 0;
+      k_macro<double><<<grid, 128, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, z0, f[0], f[1],
+                                                   f[2], f[3]);
+  };
+  auto consume = [&](int, int z0, int nzc, const char* pin) {
+    const long long C = (long long)nzc * pn;
+    std::vector<std::pair<char*, const char*>> ds;
+    std::vector<size_t> n;
+    for (int j = 0; j < nf; ++j) {
+      ds.emplace_back((char*)(outs[which[j]] + z0 * pn), pin + (size_t)j * C * 8);
+      n.push_back((size_t)C * 8);
+    }
+    par_copy(ds, n);
+  };
+  return pipelined_d2h(h, 8LL * nf, launch, consume);
 }
 
 int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz) {
@@ -2138,6 +2235,28 @@ static int pdf_io(lbm_t* h, int which, void* host, bool get) {
   if (e != cudaSuccess) return fail(LBM_ENOMEM, "pdf staging: %s", cudaGetErrorString(e));
   void* buf = which == 0 ? pre_buf(h) : h->f[1 - h->parity];
   char* hb = (char*)host;
+  if (get) {
+    cudaFree(d);
+    // pipelined: chunk = (19, nzc * pn) in the storage type
+    auto launch = [&](int, int z0, int nzc, char* dev) {
+      const dim3 grid((g.nx + 127) / 128, g.ny, nzc);
+      if (es == 4)
+        k_get_pdf<float><<<grid, 128, 0, h->stream>>>((const float*)buf, h->flags, h->sm, g, z0, (float*)dev);
+      else
+        k_get_pdf<double><<<grid, 128, 0, h->stream>>>((const double*)buf, h->flags, h->sm, g, z0, (double*)dev);
+    };
+    auto consume = [&](int, int z0, int nzc, const char* pin) {
+      const long long cn = pn * nzc;
+      std::vector<std::pair<char*, const char*>> ds;
+      std::vector<size_t> n;
+      for (int i = 0; i < Q; ++i) {
+        ds.emplace_back(hb + (i * N + z0 * pn) * es, pin + (size_t)i * cn * es);
+        n.push_back((size_t)cn * es);
+      }
+      par_copy(ds, n);
+    };
+    return pipelined_d2h(h, (long long)Q * es, launch, consume);
+  }
   // canonical (19, nz, ny, nx): one host block per direction and z chunk
   for (int z0 = 0; z0 < g.nz && e == cudaSuccess; z0 += cz) {
     const int nzc = g.nz - z0 < cz ? g.nz - z0 : cz;
