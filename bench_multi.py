@@ -20,7 +20,7 @@ def run_multi(args, rank, world, local):
     import torch.distributed as dist
 
     import paper_2108_13241_b200 as lb
-    from bench import BYTES_PER_NODE_F32, METRIC, ClockSampler, measured_peak
+    from bench import METRIC, PDF_BYTES_PER_NODE_F32, ClockSampler, measured_peak
     from paper_2108_13241_b200.distributed import channel_slab, connect_distributed, duct_slab
 
     if os.environ.get("LBM_BENCH_SAME_GPU") == "1":
@@ -71,7 +71,13 @@ def run_multi(args, rank, world, local):
     mlups = total_nons * args.steps / (ms_max / 1e3) / 1e6
     peak, peak_src = measured_peak()
     per_gpu_nodes = total_nons / world
-    achieved = per_gpu_nodes * BYTES_PER_NODE_F32 / (ms_max / args.steps / 1e3) / 1e9
+    # algorithmic bytes as at N = 1: 152 B per non-solid node + the flag /
+    # bitmap bytes the step reads, plus the halo planes pushed to the peers
+    meta = float(sim.stats().meta_bytes_per_step)
+    nx, ny = geom.dims[0], geom.dims[1]
+    halo = 2 * 5 * nx * ny * 4 if spec is not None else 0
+    alg = per_gpu_nodes * PDF_BYTES_PER_NODE_F32 + meta + halo
+    achieved = alg / (ms_max / args.steps / 1e3) / 1e9
     finite = True
     try:
         sim.check_finite()
@@ -90,7 +96,7 @@ def run_multi(args, rank, world, local):
             "mlups_per_gpu": mlups / world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "bytes_per_node": BYTES_PER_NODE_F32},
+                         "alg_bytes_per_gpu_launch": alg, "alg_bytes_per_node": alg / per_gpu_nodes},
             "e2e": None, "gpu_launches": int(launches), "clocks": clocks,
             "wall_s_max": wall_max, "finite": finite,
         }

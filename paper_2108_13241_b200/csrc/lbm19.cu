@@ -288,8 +288,10 @@ __global__ void k_tile_order_key(unsigned long long* __restrict__ key, int* __re
   const unsigned tx = tiles[3 * r], ty = tiles[3 * r + 1], tz = tiles[3 * r + 2];
   if (mode == 1)
     key[r] = spread3(tx) | spread3(ty) << 1 | spread3(tz) << 2;
-  else
+  else if (mode == 2)
     key[r] = ((((unsigned long long)(ty / B) * g.gz + tz) * B + ty % B) * g.gx) + tx;
+  else  // mode 3: z-groups of B tile layers interleaved, (tz / B, ty, tx, tz % B)
+    key[r] = ((((unsigned long long)(tz / B) * g.gy + ty) * g.gx + tx) * B) + tz % B;
   val[r] = (int)r;
 }
 
@@ -920,13 +922,15 @@ struct TileUp {
     czp = lz == g.ez - 1 ? 9 : 0, lzp = brick_z(g, lz == g.ez - 1 ? 0 : lz + 1);
     lx0 = brick_x(g, lx), ly0 = brick_y(g, ly), lz0 = brick_z(g, lz);
   }
-  __device__ __forceinline__ int at(const int* srel, int i) const {
-    const int code = 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) +
-                     (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) + (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
-    const int loc = (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) + (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
-                    (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
-    return srel[code] + loc;
+  __device__ __forceinline__ int code(int i) const {
+    return 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) + (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
+           (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
   }
+  __device__ __forceinline__ int loc(int i) const {
+    return (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) + (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
+           (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
+  }
+  __device__ __forceinline__ int at(const int* srel, int i) const { return srel[code(i)] + loc(i); }
 };
 
 // stage the 27 neighbour ranks as relative element offsets (absent: 0, i.e.
@@ -1090,6 +1094,81 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
   }
 }
 
+// Warp work list (MODE 5): one warp per group of live bricks of one tile
+// (32 lanes = 4 fp32 bricks), items t * 16 + g from a precomputed list, so no
+// lane idles for a tile's dead bricks or its last partial pass and no CTA
+// slot is held by a nearly empty tile.  The 27 neighbour offsets live in
+// lanes 0-26 and are fetched with shuffles.
+template <typename T, int TN, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
+               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+               const uint32_t* __restrict__ bmask, const int* __restrict__ items, int n_items) {
+  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wid >= n_items) return;  // whole warps
+  const int item = __ldg(items + wid);
+  const int t = item >> 4, grp = item & 15;
+  int srel = 0;
+  if (lane < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + lane);
+    srel = v < 0 ? 0 : (v - t) * (Q * TN);
+  }
+  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
+  // live-brick ordinal of this lane -> brick index (128-bit mask, words 0-3)
+  uint32_t m[4];
+  int pre_cnt[4], acc = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    m[q] = __ldg(bmask + 8LL * t + q);
+    pre_cnt[q] = acc;
+    acc += __popc(m[q]);
+  }
+  const int j = (grp << (5 - lbn)) + (lane >> lbn);
+  const bool in = j < acc;
+  int q = 3;
+  if (j < pre_cnt[3]) q = 2;
+  if (j < pre_cnt[2]) q = 1;
+  if (j < pre_cnt[1]) q = 0;
+  const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
+  const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
+  const int b = in ? q * 32 + (int)__fns(mq, 0, j - pq + 1) : 0;
+  const int l = (b << lbn) | (lane & (bn - 1));
+  const uint32_t uq = __ldg(bmask + 8LL * t + 4 + (b >> 5));
+  const bool uniform = in && ((uq >> (b & 31)) & 1u);
+  const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
+  const bool live = flag_type(w) != SOLID;
+  const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
+  T* __restrict__ tp = post + (size_t)t * (Q * TN);
+  // every lane must take part in the shuffles: dead lanes compute garbage
+  // addresses they never use
+  const TileUp up(g, l);
+  int off[Q];
+#pragma unroll
+  for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
+  if (!live) {
+    if (zfill && in) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+    }
+    return;
+  }
+  const uint32_t miss = ~w & kMaskBits;
+  T f[Q];
+  f[0] = __ldg(tb + l);
+#pragma unroll
+  for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + off[i]);
+  if (miss) {
+#pragma unroll
+    for (int i = 1; i < Q; ++i)
+      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
+  }
+  bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+}
+
 // A-A in place over the tile list (see k_step_dense_aa for the scheme):
 // NB = 1 pulls F[opp(i)] at x - c_i and pushes to F[i] at x + c_i through
 // the neighbour table; NB = 0 is node-local.
@@ -1156,8 +1235,10 @@ struct lbm_handle {
   int* nbr27 = nullptr;   // (T, 27)
   int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
   void* gh[2] = {nullptr, nullptr};  // tile slabs: ghost planes per buffer, [lo | hi] x 5 x ny x nx
+  int* items = nullptr;   // warp work list (tile << 4 | live-brick group), MODE 5
+  int n_items = 0;
   bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
-  int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows
+  int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows, 3 z-groups of `pencil` layers
   int pencil = 4;
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
   uint32_t* ubits = nullptr;  // dense: uniform-chunk bitmap (1 bit per 32 nodes)
@@ -1255,6 +1336,9 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->tiles);
   dev_free(h->nbr27);
   dev_free(h->order);
+  dev_free(h->items);
+  h->items = nullptr;
+  h->n_items = 0;
   dev_free(h->gh[0]);
   dev_free(h->gh[1]);
   h->gh[0] = h->gh[1] = nullptr;
@@ -1371,6 +1455,13 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   }
   // the select variants need more registers than the speculative gather
   constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;
+  if (var == 5) {
+    constexpr int MW = sizeof(T) == 4 ? 6 : 3;
+    if (h->n_items)
+      k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
+          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items);
+    return;
+  }
   if (var == 3)
     k_step_tiles<T, TN, 3, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
   else if (var == 4)
@@ -1565,8 +1656,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     h->use_ubits = !(ub && ub[0] == '0');
     const char* to = getenv("LBM_TILE_ORDER");  // "row": launch tiles in rank order
     // "morton" | "pencil[:B]" | "row" (rank order)
-    h->order_mode = !to ? 0 : to[0] == 'm' ? 1 : to[0] == 'p' ? 2 : 0;
-    if (to && to[0] == 'p' && strchr(to, ':')) h->pencil = atoi(strchr(to, ':') + 1) > 0 ? atoi(strchr(to, ':') + 1) : 4;
+    h->order_mode = !to ? 0 : to[0] == 'm' ? 1 : to[0] == 'p' ? 2 : to[0] == 'z' ? 3 : 0;
+    if (to && strchr(to, ':')) h->pencil = atoi(strchr(to, ':') + 1) > 0 ? atoi(strchr(to, ':') + 1) : 4;
     const char* gv = getenv("LBM_GRAPH");
     h->use_graph = !(gv && gv[0] == '0');
   }
@@ -1818,6 +1909,20 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         CK(cudaStreamSynchronize(h->stream));
         long long live = 0, uni = 0;
         for (size_t k = 0; k < hb.size(); ++k) (k % 8 < 4 ? live : uni) += __builtin_popcount(hb[k]);
+        // warp work list: groups of (32 / bricksize) live bricks per tile
+        {
+          const int per = 32 / bn;
+          std::vector<int> it;
+          it.reserve((size_t)(live / per + T));
+          for (long long t = 0; t < T; ++t) {
+            int nl = 0;
+            for (int q = 0; q < 4; ++q) nl += __builtin_popcount(hb[8 * t + q]);
+            for (int gi = 0; gi * per < nl; ++gi) it.push_back((int)(t << 4 | gi));
+          }
+          h->n_items = (int)it.size();
+          if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 1) * 4))) goto done;
+          if (!it.empty()) CK(cudaMemcpy(h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
+        }
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag words
         h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4;
       }
