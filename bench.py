@@ -330,6 +330,7 @@ def main():
         t0 = time.perf_counter()
         s2 = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
                            scheme=scheme, tile=tile)
+        t_setup = time.perf_counter() - t0
         s2.initialize(rho0)
         s2.step(args.steps)
         fields = s2.density_field() if big else s2.macroscopic_fields()
@@ -338,7 +339,10 @@ def main():
                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                "what": "Simulation(geometry) [descriptor upload] + initialize + step(K) + "
                        + ("density_field() [f64 rho readback]" if big else
-                          "macroscopic_fields() [f64 rho,u readback]") + ", wall clock"}
+                          "macroscopic_fields() [f64 rho,u readback]") + ", wall clock",
+               # the device geometry pipeline: descriptor upload, flag words,
+               # tile keep/scan/compaction/nbr27, brick masks
+               "setup_s": t_setup, "setup_mnodes_per_s": nx * ny * nz / t_setup / 1e6}
         del fields
         s2.close()
 

@@ -139,6 +139,12 @@ int lbm_set_omega(lbm_t* h, double omega);
 
 /* f64 (nz, ny, nx) arrays; solid nodes report 0. Any pointer may be NULL. */
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz);
+/* Device-side probe: the same fields on the box [lo, hi) (x, y, z order),
+ * returned as (hi_z-lo_z, hi_y-lo_y, hi_x-lo_x) arrays -- observers read a
+ * line or plane without pulling the whole domain (reference observers read
+ * the full field per call, kernel.py:262-273). */
+int lbm_get_macroscopic_box(lbm_t* h, const int32_t* lo, const int32_t* hi, double* rho,
+                            double* ux, double* uy, double* uz);
 /* Returns LBM_EDIVERGED and fills dir / node (x, y, z) when a non-finite value
  * sits in `pre`; 0 (dir = -1) otherwise. Order: direction, then visit order. */
 int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz);

@@ -61,6 +61,7 @@ SIGNATURES = [
     ("lbm_synchronize", C.c_int, [P]),
     ("lbm_set_omega", C.c_int, [P, D]),
     ("lbm_get_macroscopic", C.c_int, [P, P, P, P, P]),
+    ("lbm_get_macroscopic_box", C.c_int, [P, P, P, P, P, P, P]),
     ("lbm_check_finite", C.c_int, [P, C.POINTER(I32), P]),
     ("lbm_total_mass", C.c_int, [P, PD]),
     ("lbm_get_pdf", C.c_int, [P, I32, P]),

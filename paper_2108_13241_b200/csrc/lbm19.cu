@@ -385,12 +385,15 @@ __global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, 
 template <typename T>
 __global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
                         Geo g, int z0, double* __restrict__ rho, double* __restrict__ ux,
-                        double* __restrict__ uy, double* __restrict__ uz) {
-  // planes z0 .. z0 + gridDim.z - 1 into a staging chunk
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z + z0;
-  if (x >= g.nx) return;
-  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
+                        double* __restrict__ uy, double* __restrict__ uz, int bx0 = 0, int by0 = 0,
+                        int bnx = -1) {
+  // box [bx0, bx0 + bnx) x [by0, by0 + gridDim.y) x [z0, z0 + gridDim.z) into
+  // a staging chunk (the whole x/y extent by default)
+  if (bnx < 0) bnx = g.nx;
+  const int lx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lx >= bnx) return;
+  const int x = bx0 + lx, y = by0 + blockIdx.y, z = blockIdx.z + z0;
+  const long long n = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * bnx + lx;
   const long long s = sm.slot(g, x, y, z);
   double r = 0, vx = 0, vy = 0, vz = 0;
   const uint32_t w = s >= 0 ? flags[sm.flag_index(g, s)] : 0u;
@@ -2256,6 +2259,41 @@ int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* u
     par_copy(ds, n);
   };
   return pipelined_d2h(h, 8LL * nf, launch, consume);
+}
+
+int lbm_get_macroscopic_box(lbm_t* h, const int32_t* lo, const int32_t* hi, double* rho, double* ux,
+                            double* uy, double* uz) {
+  if (!h || !lo || !hi) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
+  const int n3[3] = {h->g.nx, h->g.ny, h->g.nz};
+  for (int a = 0; a < 3; ++a)
+    if (lo[a] < 0 || hi[a] > n3[a] || lo[a] >= hi[a])
+      return fail(LBM_EINVAL, "box [%d, %d) outside axis %d of extent %d", lo[a], hi[a], a, n3[a]);
+  DeviceGuard dg(h->d.device);
+  const Geo g = rb_geo(h);
+  const int bx = hi[0] - lo[0], by = hi[1] - lo[1], bz = hi[2] - lo[2];
+  if (by > 65535 || bz > 65535) return fail(LBM_EINVAL, "box too tall for one launch");
+  const long long C = (long long)bx * by * bz;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, C * 8 * 4);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "box readback: %s", cudaGetErrorString(e));
+  double* outs[4] = {rho, ux, uy, uz};
+  double* f[4];
+  for (int k = 0; k < 4; ++k) f[k] = outs[k] ? d + k * C : nullptr;
+  const dim3 grid((bx + 127) / 128, by, bz);
+  if (h->esize == 4)
+    k_macro<float><<<grid, 128, 0, h->stream>>>((const float*)pre_buf(h), h->flags, h->sm, g, lo[2], f[0], f[1], f[2],
+                                                f[3], lo[0], lo[1], bx);
+  else
+    k_macro<double><<<grid, 128, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, lo[2], f[0], f[1],
+                                                 f[2], f[3], lo[0], lo[1], bx);
+  e = cudaGetLastError();
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    if (outs[k]) e = cudaMemcpyAsync(outs[k], d + k * C, C * 8, cudaMemcpyDeviceToHost, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "box readback: %s", cudaGetErrorString(e));
+  return 0;
 }
 
 int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz) {

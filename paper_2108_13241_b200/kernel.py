@@ -420,6 +420,29 @@ class Simulation:
         _lib.check(h.lib.lbm_get_macroscopic(h.h, *[_lib.ptr(a) for a in out]))
         return tuple(out)
 
+    def macroscopic_box(self, x=None, y=None, z=None):
+        """(rho, v_x, v_y, v_z) on the sub-box x=(x0, x1), y=..., z=...
+        (half-open, default whole axis), computed on the device; arrays
+        shaped (z1-z0, y1-y0, x1-x0).  Observers use it to probe lines and
+        planes without downloading the domain."""
+        self.field.flush()
+        dims = self.geometry.dims
+        lo, hi = [], []
+        for a, r in enumerate((x, y, z)):
+            r = (0, dims[a]) if r is None else ((int(r), int(r) + 1) if np.isscalar(r) else r)
+            lo.append(int(r[0]))
+            hi.append(int(r[1]))
+        shape = (hi[2] - lo[2], hi[1] - lo[1], hi[0] - lo[0])
+        if min(shape) <= 0:
+            raise ValueError(f"empty box {lo} .. {hi}")
+        out = [np.empty(shape) for _ in range(4)]
+        lo_a = np.asarray(lo, dtype=np.int32)
+        hi_a = np.asarray(hi, dtype=np.int32)
+        h = self._handle
+        _lib.check(h.lib.lbm_get_macroscopic_box(h.h, _lib.ptr(lo_a), _lib.ptr(hi_a),
+                                                 *[_lib.ptr(a) for a in out]), "macroscopic_box")
+        return tuple(out)
+
     def density_field(self):
         """Per-node rho only, float64 (n_z, n_y, n_x) -- a quarter of the
         macroscopic_fields() readback, for domains near the host-memory limit."""

@@ -25,9 +25,11 @@ def centerline_profiles(simulation, z=None):
     zc = n_z // 2 if z is None else int(z)
     U = simulation.params.U
     scale = 1.0 / U if U else 1.0
-    rho, vx, vy, vz = simulation.macroscopic_fields()
-    return CenterlineProfiles(y=np.arange(n_y) / (n_y - 1), vx=vx[zc, :, n_x // 2] * scale,
-                              x=np.arange(n_x) / (n_x - 1), vy=vy[zc, n_y // 2, :] * scale)
+    # two line probes on the device instead of the whole field
+    _, vx, _, _ = simulation.macroscopic_box(x=n_x // 2, z=zc)
+    _, _, vy, _ = simulation.macroscopic_box(y=n_y // 2, z=zc)
+    return CenterlineProfiles(y=np.arange(n_y) / (n_y - 1), vx=vx[0, :, 0] * scale,
+                              x=np.arange(n_x) / (n_x - 1), vy=vy[0, 0, :] * scale)
 
 
 @dataclass

@@ -264,3 +264,24 @@ def test_channel_poiseuille_profile():
     fit = lb.poiseuille_fit(vx[2, :, 60])
     assert fit.residual <= 1e-3
     assert fit.v_max > 0
+
+
+@pytest.mark.parametrize("layout,scheme", [("dense", "ab"), ("pointer_tile", "ab"), ("dense", "aa"),
+                                           ("pointer_tile", "aa")])
+def test_macroscopic_box_probe_matches_full_readback(layout, scheme):
+    """Device-side probes (lines, planes, boxes) equal the slices of the full
+    readback, in both AA phases."""
+    c = random_mixed_geometry3(6, n=(21, 13, 11))
+    sim = lb.Simulation(to_geometry(c), params_for(1.2), layout=layout, scalar=np.float64,
+                        scheme=scheme)
+    sim.initialize(1.0)
+    for n in (3, 2):
+        sim.step(n)
+        full = sim.macroscopic_fields()
+        for box, sl in (((5, None, 4), np.s_[4:5, :, 5:6]), ((None, 7, 10), np.s_[10:11, 7:8, :]),
+                        (((2, 19), (1, 12), (3, 9)), np.s_[3:9, 1:12, 2:19])):
+            got = sim.macroscopic_box(*box)
+            for a, b in zip(got, full):
+                assert np.array_equal(a, b[sl])
+    with pytest.raises(ValueError):
+        sim.macroscopic_box(x=(4, 40))
