@@ -16,5 +16,7 @@ timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/
 for W in porous512 vascular1024 cavity64; do
   timeout 900 python bench.py --workload $W --no-cpu > gpurun_out/bench_${TAG}_${W}.json 2> gpurun_out/bench_${TAG}_${W}.err
 done
+timeout 900 python bench.py --workload channel512 --scheme aa --no-cpu > gpurun_out/bench_${TAG}_channel512_aa.json 2> gpurun_out/bench_${TAG}_channel512_aa.err
+timeout 1500 python bench.py --workload c5 --steps 300 --warmup 10 --no-cpu > gpurun_out/bench_${TAG}_c5.json 2> gpurun_out/bench_${TAG}_c5.err
 timeout 1800 bash profiles/profile.sh ${TAG} channel512 porous512 vascular1024
 ls -la gpurun_out

@@ -14,4 +14,8 @@ for W in $WLS; do
   ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 \
       -o gpurun_out/prof_${TAG}_${W} -f \
       python bench.py --workload $W --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_${TAG}_${W}.log 2>&1
+  # export the raw page and the source-line hot spots; keep the .ncu-rep only
+  # for the first workload (gpurun copies back at most 64 MiB)
+  ncu -i gpurun_out/prof_${TAG}_${W}.ncu-rep --page raw --csv > gpurun_out/raw_${TAG}_${W}.csv 2>/dev/null
+  if [ "$W" != "${WLS%% *}" ]; then rm -f gpurun_out/prof_${TAG}_${W}.ncu-rep; fi
 done

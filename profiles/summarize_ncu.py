@@ -37,8 +37,13 @@ UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12
 
 
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    """Rows of `ncu -i rep --page raw --csv`; `rep` may also be that CSV,
+    exported on the GPU box (profile.sh) so the large .ncu-rep stays there."""
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units = rows[0], rows[1]
     out = []
@@ -67,6 +72,8 @@ def main():
           "issue active % | L2 hit % | tensor pipe % |", "|---|---|---|---|---|---|---|---|---|---|"]
     for w in wls:
         rep = os.path.join(OUT, f"prof_{tag}_{w}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(OUT, f"raw_{tag}_{w}.csv")
         if not os.path.exists(rep):
             continue
         k = raw(rep)[0]
