@@ -29,6 +29,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <unistd.h>
 #include <string>
@@ -1748,6 +1749,25 @@ void lbm_destroy(lbm_t* h) {
   delete h;
 }
 
+// LBM_TIMING=1: phase times of lbm_set_geometry on stderr (device synchronised)
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTimer(cudaStream_t s) : st(s) {
+    const char* v = getenv("LBM_TIMING");
+    on = v && v[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[lbm timing] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
 int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const int32_t* bc_index,
                      const uint8_t* ghost_lo, const uint8_t* ghost_hi, const uint8_t* bc_kind,
                      const double* bc_vel, const double* bc_rho, int32_t nb) {
@@ -1767,10 +1787,12 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
   int *keep = nullptr, *scan = nullptr;
   void* cub_tmp = nullptr;
   const int nbt = nb > 0 ? nb : 1;
+  PhaseTimer pt(h->stream);
   // temporaries
   if ((rc = dev_alloc(h, &dtype_, N)) || (rc = dev_alloc(h, &dorient, N)) ||
       (rc = dev_alloc(h, &dbc, N * 4)) || (rc = dev_alloc(h, &derr, 16)))
     goto done;
+  pt.mark("alloc temporaries");
   CK(cudaMemcpyAsync(dtype_, type, N, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(dorient, orient, N, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemcpyAsync(dbc, bc_index, N * 4, cudaMemcpyHostToDevice, h->stream));
@@ -1845,6 +1867,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           (rc = dev_alloc(h, &scan, G * 4)))
         goto done;
       const int keep_all = h->d.layout == LBM_LAYOUT_TILE;
+      pt.mark("upload descriptors");
       k_tile_keep<<<(unsigned)((G * 32 + 255) / 256), 256, 0, h->stream>>>(keep, dtype_, g, keep_all, G);
       CKL();
       size_t tmp_bytes = 0;
@@ -1862,6 +1885,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       if ((rc = dev_alloc(h, &h->tiles, (T > 0 ? T : 1) * 3 * 4)) ||
           (rc = dev_alloc(h, &h->nbr27, (T > 0 ? T : 1) * 27 * 4)))
         goto done;
+      pt.mark("tile keep + scan");
       k_tile_compact<<<(unsigned)((G + 255) / 256), 256, 0, h->stream>>>(h->rank, keep, scan, h->tiles, g, G);
       CKL();
       if (T > 0) {
@@ -1893,6 +1917,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       h->nflags = h->n_slots;
       if ((rc = dev_alloc(h, &h->flags, (h->nflags > 0 ? h->nflags : 1) * 4))) goto done;
       if (h->nflags > 0) {
+        pt.mark("compact + nbr27 + order");
         k_flags_tile<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(
             h->flags, h->tiles, dtype_, dorient, dbc, glo, ghi, g, h->nflags, nb, derr, h->uscratch);
         CKL();
@@ -1907,6 +1932,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       }
       if (!h->use_ubits) CK(cudaMemset2DAsync(h->bmask + 4, 32, 0, 16, (T > 0 ? T : 1), h->stream));
       {
+        pt.mark("flags + brick masks");
         std::vector<uint32_t> hb((T > 0 ? T : 1) * 8);
         CK(cudaMemcpyAsync(hb.data(), h->bmask, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -1922,6 +1948,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
             for (int q = 0; q < 4; ++q) nl += __builtin_popcount(hb[8 * t + q]);
             for (int gi = 0; gi * per < nl; ++gi) it.push_back((int)(t << 4 | gi));
           }
+          pt.mark("brick masks to host + work list");
           h->n_items = (int)it.size();
           if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 1) * 4))) goto done;
           if (!it.empty()) CK(cudaMemcpy(h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
@@ -1956,6 +1983,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       dev_free(*p);
       *p = nullptr;
     }
+    pt.mark("geometry done");
     // PDF buffers
     const size_t fbytes = (size_t)Q * (size_t)(g.ps > 0 ? g.ps : 64) * h->esize;
     if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes))) goto done;
@@ -1963,6 +1991,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->stream));
     if (h->f[1]) CK(cudaMemsetAsync(h->f[1], 0, fbytes, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    pt.mark("PDF buffers alloc + zero");
     h->geometry = true;
     h->parity = 0;
     h->step_count = h->visited_total = 0;
