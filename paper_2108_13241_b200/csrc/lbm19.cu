@@ -1098,6 +1098,85 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
   }
 }
 
+// Shared-memory tile staging (MODE 6): pass 1 stages the tile's live bricks
+// (each thread its own nodes' 19 values, coalesced) in shared memory; after
+// one barrier, pass 2 gathers in-tile upstream values from shared memory and
+// only face links from global memory (the neighbour tiles, mostly L2 hits).
+// This cuts the L1 -> L2 sector traffic of the brick-shifted gathers, which
+// is 2-3x the DRAM traffic in the direct kernel.
+template <typename T, int TN, int MINB>
+__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
+k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
+               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+               const uint32_t* __restrict__ bmask) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  constexpr int IT = TN / BT;  // passes per thread
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sf = reinterpret_cast<T*>(smem_raw);  // [Q][TN], same order as the tile block
+  __shared__ int srel[27];
+  const int t = blockIdx.x;
+  stage_nbr<TN>(srel, nbr27, t);
+  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
+  T* __restrict__ tp = post + (size_t)t * (Q * TN);
+  const TileBricks tw(bmask, t, g, TN, true);
+  int ls[IT];
+  uint32_t ws[IT];
+  bool ins[IT];
+#pragma unroll
+  for (int p = 0; p < IT; ++p) {
+    const int k = threadIdx.x + p * BT;
+    ins[p] = false;
+    ls[p] = 0;
+    ws[p] = 0u;
+    if (k < tw.work) {
+      bool in;
+      const int l = tw.slot(k, in);
+      ls[p] = l;
+      ins[p] = in;
+      ws[p] = tw.flag(flags, t, TN, l, in);
+      if (in) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) sf[i * TN + l] = __ldg(tb + i * TN + l);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < IT; ++p) {
+    const int k = threadIdx.x + p * BT;
+    if (k >= tw.work) break;  // whole warps (work is a multiple of 32)
+    const int l = ls[p];
+    const uint32_t w = ws[p];
+    const bool live = flag_type(w) != SOLID;
+    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+    if (!live) {
+      if (zfill && ins[p]) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+      }
+      continue;
+    }
+    const uint32_t miss = ~w & kMaskBits;
+    const TileUp up(g, l);
+    T f[Q];
+    f[0] = sf[l];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      const int c = up.code(i);
+      // in-tile upstream (code 13) from shared memory, face links from global
+      f[i] = c == 13 ? sf[i * TN + up.loc(i)] : __ldg(tb + srel[c] + i * TN + up.loc(i));
+    }
+    if (miss) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = sf[opp(i) * TN + l];
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+  }
+}
+
 // Warp work list (MODE 5): one warp per group of live bricks of one tile
 // (32 lanes = 4 fp32 bricks), items t * 16 + g from a precomputed list, so no
 // lane idles for a tile's dead bricks or its last partial pass and no CTA
@@ -1459,6 +1538,18 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   }
   // the select variants need more registers than the speculative gather
   constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;
+  if (var == 6) {
+    constexpr int SMEM = Q * TN * (int)sizeof(T);
+    constexpr int MSM = (200 * 1024) / (SMEM + 512) > 0 ? (200 * 1024) / (SMEM + 512) : 1;
+    constexpr int MB = MSM < M ? MSM : M;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_step_tiles_s<T, TN, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    k_step_tiles_s<T, TN, MB><<<nt, BT, SMEM, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+    return;
+  }
   if (var == 5) {
     constexpr int MW = sizeof(T) == 4 ? 6 : 3;
     if (h->n_items)
