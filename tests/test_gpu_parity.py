@@ -285,3 +285,107 @@ def test_macroscopic_box_probe_matches_full_readback(layout, scheme):
                 assert np.array_equal(a, b[sl])
     with pytest.raises(ValueError):
         sim.macroscopic_box(x=(4, 40))
+
+
+def _open_box(n):
+    types = np.full((n, n, n), lb.NodeType.FLUID, dtype=np.uint8)
+    return lb.from_arrays("open", types)
+
+
+@pytest.mark.parametrize("v0", [(0.05, 0.0, 0.0), (0.03, -0.02, 0.01)])
+def test_uniform_motion_interior_node_unchanged_by_one_step(v0):
+    """3-D analogue of t/test_kernel.py:69-82: a uniform field advected onto
+    itself; interior nodes see identical neighbours."""
+    sim = lb.Simulation(_open_box(12), lb.FlowParams.from_viscosity(U=0.05, L=11, nu=0.1),
+                        scalar=np.float64)
+    sim.initialize(rho0=1.0, v0=v0)
+    before = sim.canonical_state()
+    sim.step()
+    after = sim.canonical_state()
+    np.testing.assert_allclose(after[:, 2:-2, 2:-2, 2:-2], before[:, 2:-2, 2:-2, 2:-2], rtol=0, atol=1e-15)
+
+
+def test_single_perturbed_node_matches_plain_loop_step():
+    """3-D analogue of t/test_kernel.py:85-103 against the plain-loop oracle
+    (oracle/scalar19.py, the t/reference_lbm.py transcription)."""
+    from oracle import scalar19 as S
+    n = 5
+    geom = _open_box(n)
+    params = lb.FlowParams.from_viscosity(U=0.05, L=4, nu=0.2)
+    rho0 = np.ones((n, n, n))
+    rho0[2, 2, 2] = 1.1
+    vx0 = np.zeros((n, n, n))
+    vx0[2, 2, 2] = 0.03
+    vz0 = np.zeros((n, n, n))
+    vz0[2, 2, 2] = -0.02
+    sim = lb.Simulation(geom, params, scalar=np.float64)
+    sim.initialize(rho0=rho0, v0=(vx0, 0.0, vz0))
+    d = geom.descriptors
+    f = S.ref_initialize(d.type_tag, np.zeros((1, 3)), np.zeros(1), d.bc_index, rho0=1.0)
+    f[:, 2, 2, 2] = S.ref_equilibrium(1.1, (0.03, 0.0, -0.02))
+    for _ in range(2):
+        sim.step()
+        f = S.ref_step(f, d.type_tag, d.orientation, np.zeros((1, 3)), np.zeros(1), d.bc_index,
+                       params.omega)
+        np.testing.assert_allclose(sim.canonical_state(), f, rtol=0, atol=1e-15)
+
+
+def test_launch_configuration_does_not_change_results(monkeypatch):
+    """Analogue of t/test_kernel.py:143-156 (worker count): every step-kernel
+    variant, tile launch order, tile shape and the CUDA-graph replay give
+    bitwise-identical states."""
+    geom = lb.build_porous_random(40, 0.45, seed=5, radius_range=(3, 7), dims=(40, 32, 24))
+    params = lb.FlowParams.from_viscosity(U=0.05, L=31, nu=0.2)
+
+    def run(layout, tile=(8, 8, 8), **env):
+        for k in ("LBM_STEP_VARIANT", "LBM_TILE_ORDER", "LBM_GRAPH"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, tile=tile)
+        sim.initialize(1.005)
+        sim.step(37)
+        return sim.canonical_state()
+
+    ref = run("dense", LBM_GRAPH="0")
+    for v in ("0", "1", "2", "3"):
+        assert np.array_equal(run("dense", LBM_STEP_VARIANT=v), ref), v
+    for v in ("0", "1", "2", "3", "4", "5", "6"):
+        assert np.array_equal(run("pointer_tile", LBM_STEP_VARIANT=v), ref), v
+    for order in ("morton", "pencil:2", "z:2"):
+        assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order), ref), order
+    for tile in ((4, 8, 16), (16, 4, 8), (8, 4, 1)):
+        assert np.array_equal(run("pointer_tile", tile=tile), ref), tile
+
+
+def test_square_duct_profile_matches_analytic():
+    """3-D physics at full path (config C5's geometry): velocity inlet on the
+    BOTTOM face, pressure outlet on TOP, bounce-back duct walls.  Downstream
+    the axial profile is the fully developed square-duct solution
+    u ~ sum_{n odd} (-1)^((n-1)/2) / n^3 [1 - cosh(n pi y/a) / cosh(n pi/2)] cos(n pi x/a)
+    with the halfway bounce-back wall half a spacing outside the wall nodes."""
+    n, nz = 17, 72
+    geom = lb.build_duct_z(n, n, nz, u_in=0.02)
+    params = lb.FlowParams.from_viscosity(U=0.02, L=n, nu=0.1)
+    sim = lb.Simulation(geom, params, scalar=np.float64)
+    sim.initialize(1.0)
+    sim.step(9000)
+    _, _, _, uz = sim.macroscopic_box(z=48)
+    a = float(n)
+    xs = np.arange(n) + 0.5 - a / 2          # node centres, walls at +-a/2
+    X, Y = np.meshgrid(xs, xs, indexing="xy")
+
+    def analytic(x, y):
+        s = np.zeros_like(x)
+        for k in range(0, 40):
+            m = 2 * k + 1
+            s += (-1) ** k / m ** 3 * (1 - np.cosh(m * np.pi * y / a) / np.cosh(m * np.pi / 2)) * np.cos(m * np.pi * x / a)
+        return s
+
+    sim_p = uz[0]
+    ana = analytic(X, Y)
+    scale = float((sim_p * ana).sum() / (ana * ana).sum())
+    err = np.abs(sim_p - scale * ana).max() / np.abs(sim_p).max()
+    assert err < 0.03, err
+    # mass flux through the section equals the inflow (incompressible, steady)
+    assert abs(sim_p.sum() - 0.02 * n * n) / (0.02 * n * n) < 0.05
