@@ -69,1238 +69,11 @@ static int fail(int code, const char* fmt, ...) {
 
 #define CKL() CK(cudaGetLastError())
 
-// ------------------------------------------------------------- device params
-struct Geo {
-  int nx, ny, nz, nxp;     // extents; nxp = padded row pitch (dense)
-  long long plane;         // ny * nxp (dense)
-  long long ps;            // elements between direction planes
-  int px, py, pzw;         // periodic x, y; wrap z inside this handle
-  int tiled;               // tile layout?
-  int ex, ey, ez, lex, ley, lez;  // tile edges and their log2
-  int lbx, lby, lbz;       // log2 of the in-tile brick (one 32-B sector: 2x2x2 fp32, 2x2x1 fp64)
-  int gx, gy, gz;          // tile grid
-  int tn;                  // nodes per tile
-  int ltn;                 // log2(tn)
-  int zero_fill;           // complete mixed sectors with zeros (full-sector stores)
-  int aa;                  // LBM_SCHEME_AA: one buffer updated in place
-  int aph;                 // AA state phase (step_count mod 2), set per readback launch
-};
-
-// In-tile slot order: the tile is cut into bricks of one 32-byte sector
-// (2x2x2 fp32 / 2x2x1 fp64 nodes), bricks x-fastest, nodes x-fastest inside
-// a brick.  A sector then holds a compact brick instead of an 8-node x-row,
-// which raises the live fraction of fetched sectors on sparse geometries.
-// The order is separable: loc = bx(lx) + by(ly) + bz(lz) (disjoint bits).
-__host__ __device__ __forceinline__ int brick_x(const Geo& g, int lx) {
-  return ((lx >> g.lbx) << (g.lbx + g.lby + g.lbz)) | (lx & ((1 << g.lbx) - 1));
-}
-__host__ __device__ __forceinline__ int brick_y(const Geo& g, int ly) {
-  return ((ly >> g.lby) << (g.lex - g.lbx + g.lbx + g.lby + g.lbz)) | ((ly & ((1 << g.lby) - 1)) << g.lbx);
-}
-__host__ __device__ __forceinline__ int brick_z(const Geo& g, int lz) {
-  return ((lz >> g.lbz) << (g.lex - g.lbx + g.ley - g.lby + g.lbx + g.lby + g.lbz)) |
-         ((lz & ((1 << g.lbz) - 1)) << (g.lbx + g.lby));
-}
-__host__ __device__ __forceinline__ void brick_inv(const Geo& g, int l, int& lx, int& ly, int& lz) {
-  const int lb = g.lbx + g.lby + g.lbz;
-  const int r = l & ((1 << lb) - 1), q = l >> lb;
-  const int nbx = g.lex - g.lbx, nby = g.ley - g.lby;
-  lx = ((q & ((1 << nbx) - 1)) << g.lbx) | (r & ((1 << g.lbx) - 1));
-  ly = (((q >> nbx) & ((1 << nby) - 1)) << g.lby) | ((r >> g.lbx) & ((1 << g.lby) - 1));
-  lz = ((q >> (nbx + nby)) << g.lbz) | (r >> (g.lbx + g.lby));
-}
-
-// element index of (direction i, slot s): dense SoA i*ps + s; tiles AoSoA
-// f[tile][i][node], i.e. each tile's 19 direction blocks are contiguous
-__device__ __forceinline__ long long fidx(const Geo& g, int i, long long s) {
-  if (!g.tiled) return (long long)i * g.ps + s;
-  return ((s >> g.ltn) * Q + i) << g.ltn | (s & (g.tn - 1));
-}
-
-struct SlotMap {
-  const int* rank;  // tile rank grid (gz, gy, gx), -1 = not allocated (tile layouts)
-  __device__ __forceinline__ long long slot(const Geo& g, int x, int y, int z) const {
-    if (!g.tiled) return ((long long)(z + 1) * g.ny + y) * g.nxp + x;
-    const int tx = x >> g.lex, ty = y >> g.ley, tz = z >> g.lez;
-    const int r = rank[((long long)tz * g.gy + ty) * g.gx + tx];
-    if (r < 0) return -1;
-    const int l = brick_x(g, x & (g.ex - 1)) + brick_y(g, y & (g.ey - 1)) + brick_z(g, z & (g.ez - 1));
-    return (long long)r * g.tn + l;
-  }
-  // flag-array index of a slot (dense flags carry no ghost planes)
-  __device__ __forceinline__ long long flag_index(const Geo& g, long long s) const {
-    return g.tiled ? s : s - g.plane;
-  }
-  // slot of the neighbour x + c_i of a node whose link i is present (so the
-  // neighbour is inside the domain or across a periodic face)
-  __device__ __forceinline__ long long nbr_slot(const Geo& g, int x, int y, int z, int i) const {
-    x += cx(i);
-    y += cy(i);
-    z += cz(i);
-    if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;
-    if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
-    if (g.pzw) { if (z < 0) z += g.nz; else if (z >= g.nz) z -= g.nz; }
-    return slot(g, x, y, z);
-  }
-};
-
-// Where pre_i(x) of the reference lives (element index into the buffer).
-// AB: the pre buffer itself.  AA (one buffer F, in place):
-//   phase 0 (even step count): pre_i(x) = F[opp(i)][x]
-//   phase 1 (odd):             pre_i(x) = F[i][x + c_i] if link i of x is
-//                              present, else F[opp(i)][x]
-// (see k_step_dense_aa for the two steps that produce these states).
-__device__ __forceinline__ long long pre_index(const Geo& g, const SlotMap& sm, int i, long long s,
-                                               uint32_t w, int x, int y, int z) {
-  if (!g.aa || i == 0) return fidx(g, i, s);
-  if (g.aph && ((w >> (i - 1)) & 1u)) return fidx(g, i, sm.nbr_slot(g, x, y, z, i));
-  return fidx(g, opp(i), s);
-}
-
-// --------------------------------------------------------------- geometry
-__device__ __forceinline__ uint32_t type_at(const uint8_t* __restrict__ type,
-                                            const uint8_t* __restrict__ glo,
-                                            const uint8_t* __restrict__ ghi, const Geo& g, int x,
-                                            int y, int z) {
-  // returns 0 (SOLID / absent) outside the domain on non-periodic axes
-  if (x < 0 || x >= g.nx) {
-    if (!g.px) return SOLID;
-    x = x < 0 ? x + g.nx : x - g.nx;
-  }
-  if (y < 0 || y >= g.ny) {
-    if (!g.py) return SOLID;
-    y = y < 0 ? y + g.ny : y - g.ny;
-  }
-  if (z < 0) return glo ? glo[(long long)y * g.nx + x] : SOLID;
-  if (z >= g.nz) return ghi ? ghi[(long long)y * g.nx + x] : SOLID;
-  return type[((long long)z * g.ny + y) * g.nx + x];
-}
-
-__device__ __forceinline__ uint32_t node_flag(const uint8_t* __restrict__ type,
-                                              const uint8_t* __restrict__ orient,
-                                              const int* __restrict__ bcidx,
-                                              const uint8_t* __restrict__ glo,
-                                              const uint8_t* __restrict__ ghi, const Geo& g,
-                                              int x, int y, int z, int nb, int* err) {
-  const long long n = ((long long)z * g.ny + y) * g.nx + x;
-  const uint32_t t = type[n];
-  const uint32_t o = orient[n];
-  const int b = bcidx[n];
-  if (t > PRESSURE_BC || o > O_BOTTOM) atomicOr(err, 1);
-  if ((t == VELOCITY_BC || t == PRESSURE_BC) && (b < 0 || b >= nb || o == O_NONE)) atomicOr(err, 2);
-  uint32_t m = 0;
-  if (t != SOLID) {
-#pragma unroll
-    for (int j = 1; j < Q; ++j)
-      if (type_at(type, glo, ghi, g, x + cx(j), y + cy(j), z + cz(j)) != SOLID) m |= 1u << (j - 1);
-  }
-  return make_flag(m, t, o, b < 0 ? 0u : (uint32_t)b);
-}
-
-// dense: one thread per (padded) flag entry
-__global__ void k_flags_dense(uint32_t* __restrict__ flags, const uint8_t* __restrict__ type,
-                              const uint8_t* __restrict__ orient, const int* __restrict__ bcidx,
-                              const uint8_t* __restrict__ glo, const uint8_t* __restrict__ ghi,
-                              Geo g, int nb, int* err, unsigned long long* nonsolid) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nxp) return;
-  uint32_t w = 0;
-  if (x < g.nx) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
-  flags[((long long)z * g.ny + y) * g.nxp + x] = w;
-  const unsigned c = __popc(__ballot_sync(0xffffffffu, flag_type(w) != SOLID));
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
-}
-
-// tiles: one warp per tile of the full tile grid -> keep flag
-__global__ void k_tile_keep(int* __restrict__ keep, const uint8_t* __restrict__ type, Geo g,
-                            int keep_all, long long ntiles) {
-  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= ntiles) return;
-  int any = 0;
-  if (keep_all) {
-    any = 1;
-  } else {
-    const int tx = (int)(t % g.gx), ty = (int)((t / g.gx) % g.gy), tz = (int)(t / ((long long)g.gx * g.gy));
-    for (int l = lane; l < g.tn && !any; l += 32) {
-      const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
-      const int x = tx * g.ex + lx, y = ty * g.ey + ly, z = tz * g.ez + lz;
-      if (x < g.nx && y < g.ny && z < g.nz && type[((long long)z * g.ny + y) * g.nx + x] != SOLID) any = 1;
-    }
-    any = __any_sync(0xffffffffu, any);
-  }
-  if (lane == 0) keep[t] = any;
-}
-
-__global__ void k_tile_compact(int* __restrict__ rank, const int* __restrict__ keep,
-                               const int* __restrict__ scan, int* __restrict__ tiles, Geo g,
-                               long long ntiles) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
-  if (keep[t]) {
-    const int r = scan[t];
-    rank[t] = r;
-    tiles[3LL * r + 0] = (int)(t % g.gx);
-    tiles[3LL * r + 1] = (int)((t / g.gx) % g.gy);
-    tiles[3LL * r + 2] = (int)(t / ((long long)g.gx * g.gy));
-  } else {
-    rank[t] = -1;
-  }
-}
-
-__global__ void k_tile_nbr(int* __restrict__ nbr, const int* __restrict__ tiles,
-                           const int* __restrict__ rank, Geo g, long long T) {
-  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= T * 27) return;
-  const long long t = k / 27;
-  const int c = (int)(k % 27);
-  const int dx = c % 3 - 1, dy = (c / 3) % 3 - 1, dz = c / 9 - 1;
-  int qx = tiles[3 * t] + dx, qy = tiles[3 * t + 1] + dy, qz = tiles[3 * t + 2] + dz;
-  int v = -1;
-  bool ok = true;
-  if (qx < 0 || qx >= g.gx) { if (g.px) qx = (qx + g.gx) % g.gx; else ok = false; }
-  if (qy < 0 || qy >= g.gy) { if (g.py) qy = (qy + g.gy) % g.gy; else ok = false; }
-  if (qz < 0 || qz >= g.gz) { if (g.pzw) qz = (qz + g.gz) % g.gz; else ok = false; }
-  if (ok) v = rank[((long long)qz * g.gy + qy) * g.gx + qx];
-  nbr[k] = v;
-}
-
-// Morton key of each kept tile (x, y, z bits interleaved), sorted to a launch
-// order: 3-D neighbours of a tile then run close in time, so the sectors they
-// share (pulled across tile faces, or pushed by the AA neighbour step) are
-// still in L2 when the second CTA touches them.  The rank order itself --
-// the reference's row-major pointer-tile order -- is unchanged.
-__device__ __forceinline__ unsigned long long spread3(unsigned v) {
-  unsigned long long x = v & 0x1fffffu;
-  x = (x | x << 32) & 0x1f00000000ffffULL;
-  x = (x | x << 16) & 0x1f0000ff0000ffULL;
-  x = (x | x << 8) & 0x100f00f00f00f00fULL;
-  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
-  x = (x | x << 2) & 0x1249249249249249ULL;
-  return x;
-}
-// mode 1: Morton; mode 2: y-pencils of B tile rows -- (y block, z, y, x) with
-// x fastest, so a tile's z neighbour runs gx*B tiles later instead of gx*gy
-__global__ void k_tile_order_key(unsigned long long* __restrict__ key, int* __restrict__ val,
-                                 const int* __restrict__ tiles, long long T, int mode, int B, Geo g) {
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= T) return;
-  const unsigned tx = tiles[3 * r], ty = tiles[3 * r + 1], tz = tiles[3 * r + 2];
-  if (mode == 1)
-    key[r] = spread3(tx) | spread3(ty) << 1 | spread3(tz) << 2;
-  else if (mode == 2)
-    key[r] = ((((unsigned long long)(ty / B) * g.gz + tz) * B + ty % B) * g.gx) + tx;
-  else  // mode 3: z-groups of B tile layers interleaved, (tz / B, ty, tx, tz % B)
-    key[r] = ((((unsigned long long)(tz / B) * g.gy + ty) * g.gx + tx) * B) + tz % B;
-  val[r] = (int)r;
-}
-
-// tiles: one thread per slot of the kept tiles
-__global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict__ tiles,
-                             const uint8_t* __restrict__ type, const uint8_t* __restrict__ orient,
-                             const int* __restrict__ bcidx, const uint8_t* __restrict__ glo,
-                             const uint8_t* __restrict__ ghi, Geo g, long long nslots, int nb,
-                             int* err, unsigned long long* nonsolid) {
-  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t w = 0;
-  if (s < nslots) {
-    const long long t = s / g.tn;
-    const int l = (int)(s - t * g.tn);
-    int lx, ly, lz;
-    brick_inv(g, l, lx, ly, lz);
-    const int x = tiles[3 * t] * g.ex + lx;
-    const int y = tiles[3 * t + 1] * g.ey + ly;
-    const int z = tiles[3 * t + 2] * g.ez + lz;
-    if (x < g.nx && y < g.ny && z < g.nz) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
-    flags[s] = w;
-  }
-  const unsigned c = __popc(__ballot_sync(0xffffffffu, s < nslots && flag_type(w) != SOLID));
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
-}
-
-// dense: bit c of the uniform-chunk bitmap is set iff the 32 nodes of warp
-// chunk c (flag index 32c .. 32c + 31) are all FLUID / BOUNCE_BACK_WALL with
-// a full neighbour mask -- such warps skip the per-node flag load
-__global__ void k_uniform_bits(uint32_t* __restrict__ ubits, const uint32_t* __restrict__ flags,
-                               long long nflags) {
-  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t w = k < nflags ? flags[k] : 0u;
-  const uint32_t t = flag_type(w);
-  const bool simple = k < nflags && (w & kMaskBits) == kMaskBits && (t == FLUID || t == BOUNCE_BACK_WALL);
-  const unsigned all = __ballot_sync(0xffffffffu, simple);
-  if ((threadIdx.x & 31) == 0 && all == 0xffffffffu) atomicOr(ubits + (k >> 10), 1u << ((k >> 5) & 31));
-}
-
-// live-brick masks: bit b of tile t is set iff brick b holds a non-solid node
-// words 0-3 of a tile: live bricks; words 4-7: uniform bricks (every node
-// FLUID / BOUNCE_BACK_WALL with a full mask: the step skips their flag words)
-__global__ void k_brick_mask(uint32_t* __restrict__ bmask, const uint32_t* __restrict__ flags, Geo g,
-                             long long nbricks) {
-  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nbricks) return;
-  const int lbn = g.lbx + g.lby + g.lbz;
-  const long long t = k >> (g.ltn - lbn);
-  const int b = (int)(k & ((g.tn >> lbn) - 1));
-  bool live = false, uni = true;
-  for (int r = 0; r < (1 << lbn); ++r) {
-    const uint32_t w = flags[(k << lbn) + r];
-    const uint32_t ty = flag_type(w);
-    live |= ty != SOLID;
-    uni &= (w & kMaskBits) == kMaskBits && (ty == FLUID || ty == BOUNCE_BACK_WALL);
-  }
-  if (live) atomicOr(bmask + 8 * t + (b >> 5), 1u << (b & 31));
-  if (uni) atomicOr(bmask + 8 * t + 4 + (b >> 5), 1u << (b & 31));
-}
-
-// ------------------------------------------------------------ init / readback
-template <typename T>
-__global__ void k_init(T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
-                       const double* __restrict__ rho, const double* __restrict__ ux,
-                       const double* __restrict__ uy, const double* __restrict__ uz, double rho0,
-                       double ux0, double uy0, double uz0, const uint8_t* __restrict__ bckind,
-                       const double* __restrict__ bcv, const double* __restrict__ bcr, int nb) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nx) return;
-  const long long s = sm.slot(g, x, y, z);
-  if (s < 0) return;
-  const uint32_t w = flags[sm.flag_index(g, s)];
-  const uint32_t t = flag_type(w);
-  if (t == SOLID) return;
-  const long long n = ((long long)z * g.ny + y) * g.nx + x;
-  double r = rho ? rho[n] : rho0, vx = ux ? ux[n] : ux0, vy = uy ? uy[n] : uy0, vz = uz ? uz[n] : uz0;
-  const int b = (int)flag_bc(w);
-  if (t == VELOCITY_BC && b < nb && bckind[b] == 0) {
-    vx = bcv[3 * b];
-    vy = bcv[3 * b + 1];
-    vz = bcv[3 * b + 2];
-  } else if (t == PRESSURE_BC && b < nb && bckind[b] == 1) {
-    r = bcr[b];
-  }
-  // AA starts in phase 0: pre_i(x) sits at F[opp(i)][x]
-#pragma unroll
-  for (int i = 0; i < Q; ++i) pre[fidx(g, g.aa ? opp(i) : i, s)] = (T)init_eq(i, r, vx, vy, vz);
-}
-
-template <typename T>
-__global__ void k_macro(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
-                        Geo g, int z0, double* __restrict__ rho, double* __restrict__ ux,
-                        double* __restrict__ uy, double* __restrict__ uz, int bx0 = 0, int by0 = 0,
-                        int bnx = -1) {
-  // box [bx0, bx0 + bnx) x [by0, by0 + gridDim.y) x [z0, z0 + gridDim.z) into
-  // a staging chunk (the whole x/y extent by default)
-  if (bnx < 0) bnx = g.nx;
-  const int lx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lx >= bnx) return;
-  const int x = bx0 + lx, y = by0 + blockIdx.y, z = blockIdx.z + z0;
-  const long long n = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * bnx + lx;
-  const long long s = sm.slot(g, x, y, z);
-  double r = 0, vx = 0, vy = 0, vz = 0;
-  const uint32_t w = s >= 0 ? flags[sm.flag_index(g, s)] : 0u;
-  if (s >= 0 && flag_type(w) != SOLID) {
-    double f[Q];
-#pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = (double)pre[pre_index(g, sm, i, s, w, x, y, z)];
-    using A = ar<double>;
-    r = density19(f);
-    if (r != 0.0) {
-      double mx, my, mz;
-      momentum19(f, mx, my, mz);
-      vx = A::div(mx, r);
-      vy = A::div(my, r);
-      vz = A::div(mz, r);
-    }
-  }
-  if (rho) rho[n] = r;
-  if (ux) ux[n] = vx;
-  if (uy) uy[n] = vy;
-  if (uz) uz[n] = vz;
-}
-
-template <typename T>
-__global__ void k_get_pdf(const T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
-                          int z0, T* __restrict__ out) {
-  // planes z0 .. z0 + gridDim.z - 1 into a (19, chunk nodes) staging block
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z + z0;
-  if (x >= g.nx) return;
-  const long long N = (long long)g.nx * g.ny * gridDim.z;
-  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
-  const long long s = sm.slot(g, x, y, z);
-  if (s < 0) {
-#pragma unroll
-    for (int i = 0; i < Q; ++i) out[i * N + n] = (T)0;
-    return;
-  }
-  const uint32_t w = flags[sm.flag_index(g, s)];
-  // AA holds only non-solid nodes' values; solid storage reads 0 either way
-  const bool live = !g.aa || flag_type(w) != SOLID;
-#pragma unroll
-  for (int i = 0; i < Q; ++i) out[i * N + n] = live ? buf[pre_index(g, sm, i, s, w, x, y, z)] : (T)0;
-}
-
-template <typename T>
-__global__ void k_set_pdf(T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
-                          int z0, const T* __restrict__ in) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z + z0;
-  if (x >= g.nx) return;
-  const long long N = (long long)g.nx * g.ny * gridDim.z;
-  const long long n = ((long long)blockIdx.z * g.ny + y) * g.nx + x;
-  const long long s = sm.slot(g, x, y, z);
-  if (s < 0) return;
-  const uint32_t w = flags[sm.flag_index(g, s)];
-  if (g.aa && flag_type(w) == SOLID) return;  // AA: solid storage is never written
-#pragma unroll
-  for (int i = 0; i < Q; ++i) buf[pre_index(g, sm, i, s, w, x, y, z)] = in[i * N + n];
-}
-
-// AA: decoded pre buffer in the native slot order (lbm_get_field / set_field)
-template <typename T, bool GET>
-__global__ void k_field_aa(T* __restrict__ buf, const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
-                           T* __restrict__ io) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nx) return;
-  const long long s = sm.slot(g, x, y, z);
-  if (s < 0) return;
-  const uint32_t w = flags[sm.flag_index(g, s)];
-  if (flag_type(w) == SOLID) return;
-#pragma unroll
-  for (int i = 0; i < Q; ++i) {
-    const long long k = pre_index(g, sm, i, s, w, x, y, z);
-    if (GET)
-      io[fidx(g, i, s)] = buf[k];
-    else
-      buf[k] = io[fidx(g, i, s)];
-  }
-}
-
-__global__ void k_slot_of(SlotMap sm, Geo g, int* __restrict__ out) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nx) return;
-  out[((long long)z * g.ny + y) * g.nx + x] = (int)sm.slot(g, x, y, z);
-}
-
-__global__ void k_get_flags(const uint32_t* __restrict__ flags, SlotMap sm, Geo g,
-                            uint32_t* __restrict__ out) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nx) return;
-  const long long s = sm.slot(g, x, y, z);
-  out[((long long)z * g.ny + y) * g.nx + x] = s >= 0 ? flags[sm.flag_index(g, s)] : 0u;
-}
-
-// first non-finite value of `pre` in (direction, visit order); visit order is
-// canonical for dense layouts and tile-major for tile layouts
-template <typename T>
-__global__ void k_nonfinite(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
-                            Geo g, long long V, unsigned long long* best) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nx) return;
-  const long long s = sm.slot(g, x, y, z);
-  if (s < 0) return;
-  const uint32_t w = flags[sm.flag_index(g, s)];
-  if (flag_type(w) == SOLID) return;
-  const long long v = g.tiled ? s : ((long long)z * g.ny + y) * g.nx + x;
-  for (int i = 0; i < Q; ++i) {
-    const T val = pre[pre_index(g, sm, i, s, w, x, y, z)];
-    if (!isfinite((double)val)) {
-      atomicMin(best, (unsigned long long)(i * V + v));
-      return;
-    }
-  }
-}
-
-// deterministic two-pass mass reduction: per-block partial sums, then one block
-template <typename T>
-__global__ void k_mass_partial(const T* __restrict__ pre, const uint32_t* __restrict__ flags, SlotMap sm,
-                               const int* __restrict__ tiles, Geo g, long long nflags,
-                               double* __restrict__ partial) {
-  __shared__ double sh[256];
-  double acc = 0.0;
-  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nflags;
-       k += (long long)gridDim.x * blockDim.x) {
-    const uint32_t w = flags[k];
-    if (flag_type(w) == SOLID) continue;
-    const long long s = g.tiled ? k : k + g.plane;
-    int x = 0, y = 0, z = 0;  // node coordinates (AA phase 1 reads neighbours)
-    if (g.aa && g.aph) {
-      if (g.tiled) {
-        const long long t = k >> g.ltn;
-        brick_inv(g, (int)(k & (g.tn - 1)), x, y, z);
-        x += tiles[3 * t] * g.ex;
-        y += tiles[3 * t + 1] * g.ey;
-        z += tiles[3 * t + 2] * g.ez;
-      } else {
-        z = (int)(k / g.plane);
-        const long long r = k - (long long)z * g.plane;
-        y = (int)(r / g.nxp);
-        x = (int)(r - (long long)y * g.nxp);
-      }
-    }
-    double a = 0.0;
-    for (int i = 0; i < Q; ++i) a += (double)pre[pre_index(g, sm, i, s, w, x, y, z)];
-    acc += a;
-  }
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
-}
-
-__global__ void k_mass_final(const double* __restrict__ partial, int n, double* out) {
-  __shared__ double sh[256];
-  double acc = 0.0;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += partial[k];
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = sh[0];
-}
-
-// ------------------------------------------------------------------ steps
-// Solid lanes complete the 32-B sectors of their non-solid neighbours with
-// zeros (the values they already hold), so every store is a full sector.
-template <typename T>
-__device__ __forceinline__ bool sector_needs_zero(bool nonsolid) {
-  constexpr int SEC = 32 / (int)sizeof(T);
-  const unsigned act = __ballot_sync(0xffffffffu, nonsolid);
-  const int lane = threadIdx.x & 31;
-  const unsigned grp = ((1u << SEC) - 1u) << (lane & ~(SEC - 1));
-  return (act & grp) != 0u;
-}
-
-// z-slab halo, fused into the step: the outgoing populations of the two
-// boundary planes (c_z = -1 from z = 0, c_z = +1 from z = nz - 1) are stored
-// straight into the neighbouring slab's ghost plane (peer memory over
-// NVLink / IPC), next to the node-local store.  Null pointers: no neighbour.
-__host__ __device__ constexpr int kZm(int j) { return 10 + 2 * j; }  // c_z = -1: 10 12 14 16 18
-__host__ __device__ constexpr int kZp(int j) { return 9 + 2 * j; }   // c_z = +1: 9 11 13 15 17
-template <typename T>
-struct Halo {
-  T* lo[5];  // lower neighbour's upper ghost plane, directions kZm
-  T* hi[5];  // upper neighbour's lower ghost plane, directions kZp
-};
-
-__global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int need_hi,
-                            unsigned long long target, int* err) {
-  const long long t0 = clock64();
-  const volatile unsigned long long* vs = sync;
-  while ((need_lo && vs[0] < target) || (need_hi && vs[1] < target)) {
-    __nanosleep(200);
-    if (clock64() - t0 > 60LL * 2000000000LL) {  // ~1 min at 2 GHz: a neighbour is gone
-      atomicOr(err, 1);
-      return;
-    }
-  }
-  __threadfence_system();
-}
-
-__global__ void k_halo_signal(unsigned long long* lo_slot, unsigned long long* hi_slot,
-                              unsigned long long value) {
-  __threadfence_system();
-  if (lo_slot) *(volatile unsigned long long*)lo_slot = value;
-  if (hi_slot) *(volatile unsigned long long*)hi_slot = value;
-  __threadfence_system();
-}
-
-// initial ghost fill (after initialize / set_pdf): boundary planes of `pre`
-template <typename T>
-__global__ void k_halo_push(const T* __restrict__ pre, Halo<T> H, Geo g) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  if (x >= g.nxp) return;
-  const int row = y * g.nxp + x;
-  const int s0 = (int)g.plane + row, s1 = g.nz * (int)g.plane + row;
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    if (H.lo[0]) H.lo[j][row] = pre[(long long)kZm(j) * g.ps + s0];
-    if (H.hi[0]) H.hi[j][row] = pre[(long long)kZp(j) * g.ps + s1];
-  }
-  __threadfence_system();
-}
-
-// 19 direction planes of one buffer, resolved on the host once per launch, so
-// every access is a 32-bit slot offset from a per-direction base pointer
-template <typename T>
-struct Planes {
-  const T* pre[Q];
-  T* post[Q];
-};
-
-template <typename T>
-__device__ __forceinline__ void bc_collide(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
-                                           const T* __restrict__ bcr, T om) {
-  const uint32_t t = flag_type(w);
-  if (t == VELOCITY_BC) {
-    const uint32_t b = flag_bc(w);
-    zou_he_velocity19<T>(f, flag_orient(w), bcv[3 * b], bcv[3 * b + 1], bcv[3 * b + 2]);
-  } else if (t == PRESSURE_BC) {
-    zou_he_pressure19<T>(f, flag_orient(w), bcr[flag_bc(w)]);
-  }
-  T rho, vx, vy, vz;
-  moments19(f, rho, vx, vy, vz);
-  collide19(f, rho, vx, vy, vz, om);
-}
-
-template <typename T>
-__device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
-                                                 const T* __restrict__ bcr, T om,
-                                                 const Planes<T>& P, unsigned s) {
-  bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-  for (int i = 0; i < Q; ++i) P.post[i][s] = f[i];
-}
-
-// Link-wise bounce-back fix-up: every f_i was loaded speculatively from the
-// upstream slot (always a valid address); where the mask bit of opp(i) is
-// clear the node reflects its own f_opp(i) instead (reference kernel.py:84-116).
-template <typename T>
-__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, const Planes<T>& P, unsigned s) {
-  if (miss) {
-#pragma unroll
-    for (int i = 1; i < Q; ++i)
-      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(P.pre[opp(i)] + s);
-  }
-}
-
-// Gather of the 18 moving populations.  MODE 0: speculative pull of every
-// upstream slot, then the fix-up for masked links.  MODE 1: warps whose live
-// nodes all have full masks pull unconditionally, the others select per link
-// so no byte is fetched for a masked link.
-template <typename T, int MODE, typename Up>
-__device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, const Planes<T>& P, unsigned s,
-                                       Up up) {
-  if (MODE == 0 || fast) {
-#pragma unroll
-    for (int i = 1; i < Q; ++i) f[i] = __ldg(P.pre[i] + up(i));
-    if (MODE == 0) bounce_back_fixup(f, miss, P, s);
-  } else {
-#pragma unroll
-    for (int i = 1; i < Q; ++i)
-      f[i] = ((miss >> (opp(i) - 1)) & 1u) ? __ldg(P.pre[opp(i)] + s) : __ldg(P.pre[i] + up(i));
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void zero_fill(const Planes<T>& P, unsigned s) {
-#pragma unroll
-  for (int i = 0; i < Q; ++i) P.post[i][s] = (T)0;
-}
-
-// dense: offsets from slot s to the upstream node x - c_i, per axis (wrap on
-// periodic axes; on closed axes the edge offset is 0 and the link is masked,
-// so the speculative address stays valid)
-struct UpOffsets {
-  unsigned xm, xp, ym, yp, zm, zp;
-  __device__ __forceinline__ UpOffsets(const Geo& g, int x, int y, int z) {
-    xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
-    xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
-    ym = y == 0 ? (g.py ? (unsigned)(g.ny - 1) * g.nxp : 0u) : (unsigned)-g.nxp;
-    yp = y == g.ny - 1 ? (g.py ? (unsigned)-((g.ny - 1) * g.nxp) : 0u) : (unsigned)g.nxp;
-    const unsigned pl = (unsigned)g.plane;
-    zm = (z == 0 && g.pzw) ? (unsigned)(g.nz - 1) * pl : 0u - pl;
-    zp = (z == g.nz - 1 && g.pzw) ? 0u - (unsigned)(g.nz - 1) * pl : pl;
-  }
-  // slot of x - c_i
-  __device__ __forceinline__ unsigned up(unsigned s, int i) const {
-    return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0u)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0u)) +
-           (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0u));
-  }
-};
-
-template <typename T, int MODE, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
-                                                   const uint32_t* __restrict__ ubits,
-                                                   const T* __restrict__ bcv,
-                                                   const T* __restrict__ bcr, Geo g, T om,
-                                                   const Halo<T> H) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
-  // 32-bit unsigned slot arithmetic (slabs up to 2^32 slots; negative
-  // offsets wrap modulo 2^32 and land on the right slot)
-  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
-  const unsigned s = fi + (unsigned)g.plane;
-  const uint32_t ub = __ldg(ubits + (fi >> 10));
-  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
-  const bool live = flag_type(w) != SOLID;
-  const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-  const uint32_t miss = ~w & kMaskBits;
-  // warps whose live nodes all have full masks pull unconditionally; the
-  // rest select per link, so no byte is fetched for a masked link
-  const bool fast = MODE == 1 && __all_sync(0xffffffffu, !live || miss == 0u);
-  if (!live) {
-    if (zfill) zero_fill(P, s);
-    return;
-  }
-  // offsets to the upstream node x - c_i along each axis (wrap on periodic
-  // axes; on closed axes the edge offset is 0 and the link is masked)
-  const UpOffsets o(g, x, y, z);
-  auto up = [&](int i) { return o.up(s, i); };
-  T f[Q];
-  f[0] = __ldg(P.pre[0] + s);
-  gather<T, MODE>(f, miss, fast, P, s, up);
-  bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
-  if ((z == 0 && H.lo[0]) || (z == g.nz - 1 && H.hi[0])) {
-    const int row = y * g.nxp + x;
-    if (z == 0 && H.lo[0]) {
-#pragma unroll
-      for (int j = 0; j < 5; ++j) H.lo[j][row] = f[kZm(j)];
-    }
-    if (z == g.nz - 1 && H.hi[0]) {
-#pragma unroll
-      for (int j = 0; j < 5; ++j) H.hi[j][row] = f[kZp(j)];
-    }
-    __threadfence_system();
-  }
-}
-
-// A-A in place (LBM_SCHEME_AA): one buffer F, two alternating kernels, each
-// node reading and writing only locations no other node touches in the same
-// launch, so no second buffer is needed.  Per reference step (pull gather of
-// the previous post-collision values, then collide; kernel.py:72-141):
-//   NB = 1 (state phase 0 -> 1), F[opp(i)][x] holds pre_i(x):
-//      f_i = F[opp(i)][x - c_i]  if link opp(i) of x is present (pre_i(x - c_i))
-//          = F[i][x]             otherwise (bounce-back: pre_opp(i)(x))
-//      store f*_i to F[i][x + c_i] if link i is present, else F[opp(i)][x]
-//   NB = 0 (phase 1 -> 0): f_i = F[i][x]; store f*_i to F[opp(i)][x]
-// F[i][x + c_i] is read (as f_opp(i)) and written by node x alone, so the
-// update is race-free; the arithmetic is the AB kernel's, bit for bit.
-template <typename T>
-struct Planes1 {
-  T* f[Q];
-};
-
-// AA loads may take the read-only (non-coherent) path: every location is
-// read and then written by one thread only, so no cached copy can be stale
-template <typename T>
-__device__ __forceinline__ T LDA(const T* p) {
-  return __ldg(p);
-}
-
-// hides a value from the optimiser: the neighbour step's store addresses are
-// the load addresses of the opposite directions, and letting the compiler
-// keep those 18 addresses live across the collision costs spills; an opaque
-// copy makes it recompute them from a handful of offsets instead
-__device__ __forceinline__ unsigned opaque(unsigned v) {
-  asm volatile("" : "+r"(v));
-  return v;
-}
-__device__ __forceinline__ int opaque(int v) {
-  asm volatile("" : "+r"(v));
-  return v;
-}
-
-template <typename T, int NB, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P, const uint32_t* __restrict__ flags,
-                                                      const uint32_t* __restrict__ ubits,
-                                                      const T* __restrict__ bcv, const T* __restrict__ bcr,
-                                                      Geo g, T om) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
-  if (x >= g.nxp) return;
-  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
-  const unsigned s = fi + (unsigned)g.plane;
-  const uint32_t ub = __ldg(ubits + (fi >> 10));
-  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
-  // no zero-fill of solid lanes here (unlike the AB kernel): every sector
-  // this step writes was read by the same step, so it sits in L2 whole and a
-  // partial store needs no DRAM read-for-merge; zero stores from solid lanes
-  // would instead race ahead of the live lanes' loads of the same sectors
-  if (flag_type(w) == SOLID) return;
-  const uint32_t miss = ~w & kMaskBits;
-  T f[Q];
-  f[0] = LDA(P.f[0] + s);
-  if (NB) {
-    const UpOffsets o(g, x, y, z);
-#pragma unroll
-    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));  // speculative, always a valid slot
-    if (miss) {
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(P.f[i] + s);
-    }
-    bc_collide<T>(f, w, bcv, bcr, om);
-    // recompute the store addresses from opaque copies (measured: keeping the
-    // 18 load addresses live at 64 registers is no faster)
-    const unsigned s2 = opaque(s);
-    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
-    P.f[0][s2] = f[0];
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-      T* dst = ((miss >> (i - 1)) & 1u) ? P.f[opp(i)] + s2 : P.f[i] + o2.up(s2, opp(i));
-      *dst = f[i];
-    }
-  } else {
-#pragma unroll
-    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[i] + s);
-    bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-    for (int i = 0; i < Q; ++i) P.f[opp(i)][s] = f[i];
-  }
-}
-
-// Sparse tiles, AoSoA storage f[tile][i][TN]: one CTA per kept tile.  All
-// addresses are 32-bit element offsets from the CTA's own tile block; the
-// upstream slot of direction i is separable per axis (tile code
-// (dx+1) + 3(dy+1) + 9(dz+1), relative tile offset from shared memory, and
-// in-tile offset lx' + ex ly' + ex ey lz'), and every own-tile access
-// (bounce-back, stores) has a compile-time offset i*TN.
-
-// Live-brick work list of one tile (MODE 2): threads cover only the tile's
-// live bricks (sector-sized bricks holding >= 1 non-solid node, a 128-bit
-// mask per tile), so a sparse tile costs lanes in proportion to its live
-// sectors, not its TN slots.  Words 4-7 of the mask mark uniform bricks
-// (all FLUID / wall with full masks) whose flag words the step skips.
-struct TileBricks {
-  uint32_t m[4], u[4];
-  int pre_cnt[4];
-  int work, lbn, bn;
-  bool dense_tile;
-  __device__ __forceinline__ TileBricks(const uint32_t* __restrict__ bmask, long long t, const Geo& g, int tn,
-                                        bool compact) {
-    lbn = g.lbx + g.lby + g.lbz;
-    bn = 1 << lbn;
-    int acc = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      u[q] = __ldg(bmask + 8LL * t + 4 + q);
-      m[q] = compact ? __ldg(bmask + 8LL * t + q) : 0u;
-      pre_cnt[q] = acc;
-      acc += __popc(m[q]);
-    }
-    work = compact ? ((acc << lbn) + 31) & ~31 : tn;  // whole warps; lanes past acc*bn idle
-    dense_tile = !compact || acc == (tn >> lbn);       // every brick live: identity mapping
-  }
-  // in-tile slot of work item k; `in` false for idle lanes past the last live brick
-  __device__ __forceinline__ int slot(int k, bool& in) const {
-    in = true;
-    if (dense_tile) return k;
-    const int j = k >> lbn;  // live-brick ordinal
-    in = j < pre_cnt[3] + __popc(m[3]);
-    int q = 3;
-    if (j < pre_cnt[3]) q = 2;
-    if (j < pre_cnt[2]) q = 1;
-    if (j < pre_cnt[1]) q = 0;
-    const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
-    const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
-    const uint32_t pos = __fns(mq, 0, j - pq + 1);
-    const int b = in ? q * 32 + (int)pos : 0;
-    return (b << lbn) | (k & (bn - 1));
-  }
-  // flag word of in-tile slot l (uniform bricks skip the load)
-  __device__ __forceinline__ uint32_t flag(const uint32_t* __restrict__ flags, long long t, int tn, int l,
-                                           bool in) const {
-    const int bb = l >> lbn;
-    const uint32_t uq = bb < 32 ? u[0] : (bb < 64 ? u[1] : (bb < 96 ? u[2] : u[3]));
-    const bool uniform = in && ((uq >> (bb & 31)) & 1u);
-    return uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * tn + l) : 0u);
-  }
-};
-
-// offset (from the own tile's block, excluding the direction plane) of the
-// node x - c_i: neighbour tile from the shared relative-offset table,
-// in-tile position from the separable brick order
-struct TileUp {
-  int cxm, lxm, cxp, lxp, cym, lym, cyp, lyp, czm, lzm, czp, lzp, lx0, ly0, lz0;
-  __device__ __forceinline__ TileUp(const Geo& g, int l) {
-    int lx, ly, lz;
-    brick_inv(g, l, lx, ly, lz);
-    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, in-tile offset)
-    cxm = lx == 0 ? -1 : 0, lxm = brick_x(g, lx == 0 ? g.ex - 1 : lx - 1);
-    cxp = lx == g.ex - 1 ? 1 : 0, lxp = brick_x(g, lx == g.ex - 1 ? 0 : lx + 1);
-    cym = ly == 0 ? -3 : 0, lym = brick_y(g, ly == 0 ? g.ey - 1 : ly - 1);
-    cyp = ly == g.ey - 1 ? 3 : 0, lyp = brick_y(g, ly == g.ey - 1 ? 0 : ly + 1);
-    czm = lz == 0 ? -9 : 0, lzm = brick_z(g, lz == 0 ? g.ez - 1 : lz - 1);
-    czp = lz == g.ez - 1 ? 9 : 0, lzp = brick_z(g, lz == g.ez - 1 ? 0 : lz + 1);
-    lx0 = brick_x(g, lx), ly0 = brick_y(g, ly), lz0 = brick_z(g, lz);
-  }
-  __device__ __forceinline__ int code(int i) const {
-    return 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) + (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
-           (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
-  }
-  __device__ __forceinline__ int loc(int i) const {
-    return (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) + (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
-           (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
-  }
-  __device__ __forceinline__ int at(const int* srel, int i) const { return srel[code(i)] + loc(i); }
-};
-
-// stage the 27 neighbour ranks as relative element offsets (absent: 0, i.e.
-// the own tile -- such links are masked)
-template <int TN>
-__device__ __forceinline__ void stage_nbr(int* srel, const int* __restrict__ nbr27, int t) {
-  if (threadIdx.x < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
-    srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
-}
-
-// z-slab halo for tile layouts: ghost planes (5 populations x ny x nx, row
-// pitch nx) per buffer.  pre_lo / pre_hi: this slab's ghosts of the pre
-// buffer (filled by the neighbours' previous step); push_lo / push_hi: the
-// neighbours' ghosts of the post buffer (peer memory), which this step fills
-// with the c_z = -1 / +1 populations of its bottom / top plane.
-template <typename T>
-struct TileHalo {
-  int on;
-  const int* tiles;
-  const T* pre_lo;   // kZp(j) populations of plane z = -1
-  const T* pre_hi;   // kZm(j) populations of plane z = nz
-  T* push_lo[5];     // lower neighbour's hi ghost (kZm)
-  T* push_hi[5];     // upper neighbour's lo ghost (kZp)
-};
-
-template <typename T>
-__device__ __forceinline__ long long ghost_row(const Geo& g, int x, int y) {
-  if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;  // present links wrap only on periodic axes
-  if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
-  return (long long)y * g.nx + x;
-}
-
-// links into the ghost planes replace the (meaningless) speculative values
-template <typename T>
-__device__ __forceinline__ void tile_ghost_gather(T (&f)[Q], uint32_t miss, const TileHalo<T>& TH, const Geo& g,
-                                                  int x, int y, int z) {
-  const long long pn = (long long)g.nx * g.ny;
-  if (z == 0 && TH.pre_lo) {
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const int i = kZp(j);
-      if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = __ldg(TH.pre_lo + j * pn + ghost_row<T>(g, x - cx(i), y - cy(i)));
-    }
-  }
-  if (z == g.nz - 1 && TH.pre_hi) {
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const int i = kZm(j);
-      if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = __ldg(TH.pre_hi + j * pn + ghost_row<T>(g, x - cx(i), y - cy(i)));
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void tile_ghost_push(const T (&f)[Q], const TileHalo<T>& TH, const Geo& g, int x, int y,
-                                                int z) {
-  const long long r = (long long)y * g.nx + x;
-  if (z == 0 && TH.push_lo[0]) {
-#pragma unroll
-    for (int j = 0; j < 5; ++j) TH.push_lo[j][r] = f[kZm(j)];
-    __threadfence_system();
-  }
-  if (z == g.nz - 1 && TH.push_hi[0]) {
-#pragma unroll
-    for (int j = 0; j < 5; ++j) TH.push_hi[j][r] = f[kZp(j)];
-    __threadfence_system();
-  }
-}
-
-// initial ghost fill for tile layouts: boundary planes of `pre`
-template <typename T>
-__global__ void k_tile_halo_push(const T* __restrict__ pre, SlotMap sm, Geo g, TileHalo<T> TH) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  if (x >= g.nx) return;
-  const long long r = (long long)y * g.nx + x;
-  const long long s0 = sm.slot(g, x, y, 0), s1 = sm.slot(g, x, y, g.nz - 1);
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    if (TH.push_lo[0]) TH.push_lo[j][r] = s0 >= 0 ? pre[fidx(g, kZm(j), s0)] : (T)0;
-    if (TH.push_hi[0]) TH.push_hi[j][r] = s1 >= 0 ? pre[fidx(g, kZp(j), s1)] : (T)0;
-  }
-  __threadfence_system();
-}
-
-// MODE 0: speculative pull + fix-up over all TN slots; MODE 1: select per
-// link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only;
-// MODE 3: MODE 1 over live bricks; MODE 4: live bricks, warps whose live
-// nodes all have full masks pull unconditionally, the others select per link.
-template <typename T, int TN, int MODE, int MINB, bool CUT = false>
-__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
-k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-             const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-             const uint32_t* __restrict__ bmask, const int* __restrict__ order, const TileHalo<T> TH) {
-  constexpr int BT = TN < 256 ? TN : 256;
-  __shared__ int srel[27];
-  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
-  stage_nbr<TN>(srel, nbr27, t);
-  // z-slab cut: tiles on the first / last tile plane exchange their boundary
-  // nodes' c_z populations through ghost planes (uniform per CTA)
-  int tz0 = 0, tx0 = 0, ty0 = 0;
-  bool cut = false;
-  if (CUT) {
-    tx0 = __ldg(TH.tiles + 3 * t) * g.ex;
-    ty0 = __ldg(TH.tiles + 3 * t + 1) * g.ey;
-    tz0 = __ldg(TH.tiles + 3 * t + 2) * g.ez;
-    cut = tz0 == 0 || tz0 + g.ez >= g.nz;
-  }
-  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-  T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  constexpr bool kCompact = MODE >= 2;
-  constexpr bool kSelect = MODE == 1 || MODE == 3;
-  const TileBricks tw(bmask, t, g, TN, kCompact);
-  __syncthreads();
-#pragma unroll 1
-  for (int k = threadIdx.x; k < tw.work; k += BT) {
-    bool in;
-    const int l = tw.slot(k, in);
-    const uint32_t w = tw.flag(flags, t, TN, l, in);
-    const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    const uint32_t miss = ~w & kMaskBits;
-    const bool fast = MODE == 4 ? __all_sync(0xffffffffu, !live || miss == 0u) : !kSelect;
-    if (!live) {
-      if (zfill && in) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
-      }
-      continue;
-    }
-    const TileUp up(g, l);
-    T f[Q];
-    f[0] = __ldg(tb + l);
-    if (fast) {
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + up.at(srel, i));
-      if (miss) {
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-          if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
-      }
-    } else {
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : i * TN + up.at(srel, i)));
-    }
-    int x = 0, y = 0, z = -1;
-    if (CUT && cut) {
-      brick_inv(g, l, x, y, z);
-      x += tx0;
-      y += ty0;
-      z += tz0;
-      tile_ghost_gather<T>(f, miss, TH, g, x, y, z);
-    }
-    bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
-    if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
-  }
-}
-
-// Shared-memory tile staging (MODE 6): pass 1 stages the tile's live bricks
-// (each thread its own nodes' 19 values, coalesced) in shared memory; after
-// one barrier, pass 2 gathers in-tile upstream values from shared memory and
-// only face links from global memory (the neighbour tiles, mostly L2 hits).
-// This cuts the L1 -> L2 sector traffic of the brick-shifted gathers, which
-// is 2-3x the DRAM traffic in the direct kernel.
-template <typename T, int TN, int MINB>
-__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
-k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask) {
-  constexpr int BT = TN < 256 ? TN : 256;
-  constexpr int IT = TN / BT;  // passes per thread
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sf = reinterpret_cast<T*>(smem_raw);  // [Q][TN], same order as the tile block
-  __shared__ int srel[27];
-  const int t = blockIdx.x;
-  stage_nbr<TN>(srel, nbr27, t);
-  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-  T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, true);
-  int ls[IT];
-  uint32_t ws[IT];
-  bool ins[IT];
-#pragma unroll
-  for (int p = 0; p < IT; ++p) {
-    const int k = threadIdx.x + p * BT;
-    ins[p] = false;
-    ls[p] = 0;
-    ws[p] = 0u;
-    if (k < tw.work) {
-      bool in;
-      const int l = tw.slot(k, in);
-      ls[p] = l;
-      ins[p] = in;
-      ws[p] = tw.flag(flags, t, TN, l, in);
-      if (in) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) sf[i * TN + l] = __ldg(tb + i * TN + l);
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int p = 0; p < IT; ++p) {
-    const int k = threadIdx.x + p * BT;
-    if (k >= tw.work) break;  // whole warps (work is a multiple of 32)
-    const int l = ls[p];
-    const uint32_t w = ws[p];
-    const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    if (!live) {
-      if (zfill && ins[p]) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
-      }
-      continue;
-    }
-    const uint32_t miss = ~w & kMaskBits;
-    const TileUp up(g, l);
-    T f[Q];
-    f[0] = sf[l];
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-      const int c = up.code(i);
-      // in-tile upstream (code 13) from shared memory, face links from global
-      f[i] = c == 13 ? sf[i * TN + up.loc(i)] : __ldg(tb + srel[c] + i * TN + up.loc(i));
-    }
-    if (miss) {
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        if ((miss >> (opp(i) - 1)) & 1u) f[i] = sf[opp(i) * TN + l];
-    }
-    bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
-  }
-}
-
-// Warp work list (MODE 5): one warp per group of live bricks of one tile
-// (32 lanes = 4 fp32 bricks), items t * 16 + g from a precomputed list, so no
-// lane idles for a tile's dead bricks or its last partial pass and no CTA
-// slot is held by a nearly empty tile.  The 27 neighbour offsets live in
-// lanes 0-26 and are fetched with shuffles.
-template <typename T, int TN, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask, const int* __restrict__ items, int n_items) {
-  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (wid >= n_items) return;  // whole warps
-  const int item = __ldg(items + wid);
-  const int t = item >> 4, grp = item & 15;
-  int srel = 0;
-  if (lane < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + lane);
-    srel = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
-  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  // live-brick ordinal of this lane -> brick index (128-bit mask, words 0-3)
-  uint32_t m[4];
-  int pre_cnt[4], acc = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    m[q] = __ldg(bmask + 8LL * t + q);
-    pre_cnt[q] = acc;
-    acc += __popc(m[q]);
-  }
-  const int j = (grp << (5 - lbn)) + (lane >> lbn);
-  const bool in = j < acc;
-  int q = 3;
-  if (j < pre_cnt[3]) q = 2;
-  if (j < pre_cnt[2]) q = 1;
-  if (j < pre_cnt[1]) q = 0;
-  const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
-  const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
-  const int b = in ? q * 32 + (int)__fns(mq, 0, j - pq + 1) : 0;
-  const int l = (b << lbn) | (lane & (bn - 1));
-  const uint32_t uq = __ldg(bmask + 8LL * t + 4 + (b >> 5));
-  const bool uniform = in && ((uq >> (b & 31)) & 1u);
-  const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
-  const bool live = flag_type(w) != SOLID;
-  const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-  T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  // every lane must take part in the shuffles: dead lanes compute garbage
-  // addresses they never use
-  const TileUp up(g, l);
-  int off[Q];
-#pragma unroll
-  for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
-  if (!live) {
-    if (zfill && in) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
-    }
-    return;
-  }
-  const uint32_t miss = ~w & kMaskBits;
-  T f[Q];
-  f[0] = __ldg(tb + l);
-#pragma unroll
-  for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + off[i]);
-  if (miss) {
-#pragma unroll
-    for (int i = 1; i < Q; ++i)
-      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
-  }
-  bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-  for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
-}
-
-// A-A in place over the tile list (see k_step_dense_aa for the scheme):
-// NB = 1 pulls F[opp(i)] at x - c_i and pushes to F[i] at x + c_i through
-// the neighbour table; NB = 0 is node-local.
-template <typename T, int TN, int NB, int MINB>
-__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
-k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
-                const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-                const uint32_t* __restrict__ bmask, const int* __restrict__ order) {
-  constexpr int BT = TN < 256 ? TN : 256;
-  __shared__ int srel[27];
-  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
-  if (NB) stage_nbr<TN>(srel, nbr27, t);
-  T* __restrict__ tb = F + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, true);
-  if (NB) __syncthreads();
-#pragma unroll 1
-  for (int k = threadIdx.x; k < tw.work; k += BT) {
-    bool in;
-    const int l = tw.slot(k, in);
-    const uint32_t w = tw.flag(flags, t, TN, l, in);
-    if (flag_type(w) == SOLID) continue;  // no zero-fill under AA (see k_step_dense_aa)
-    const uint32_t miss = ~w & kMaskBits;
-    T f[Q];
-    f[0] = LDA(tb + l);
-    if (NB) {
-      const TileUp up(g, l);
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + opp(i) * TN + up.at(srel, i));
-      if (miss) {
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-          if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(tb + i * TN + l);
-      }
-      bc_collide<T>(f, w, bcv, bcr, om);
-      const int l2 = opaque(l);
-      const TileUp up2(g, l2);
-      tb[l2] = f[0];
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + up2.at(srel, opp(i))] = f[i];
-    } else {
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
-      bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-      for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
-    }
-  }
-}
+#include "layout.cuh"
+#include "geometry_kernels.cuh"
+#include "readback_kernels.cuh"
+#include "step_dense.cuh"
+#include "step_tiles.cuh"
 
 // ----------------------------------------------------------------- handle
 struct lbm_handle {
@@ -1532,41 +305,47 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T om = (T)h->d.omega;
   if (TH.on) {  // z-slab: the live-brick kernel with the ghost-plane exchange
     k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
-        pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                               h->bmask, h->order, TH);
+        pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
     return;
   }
-  // the select variants need more registers than the speculative gather
-  constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;
-  if (var == 6) {
-    constexpr int SMEM = Q * TN * (int)sizeof(T);
-    constexpr int MSM = (200 * 1024) / (SMEM + 512) > 0 ? (200 * 1024) / (SMEM + 512) : 1;
-    constexpr int MB = MSM < M ? MSM : M;
-    static bool attr = false;
-    if (!attr) {
+  // measured alternatives (LBM_STEP_VARIANT, profiles/sparse_r01.md), built
+  // for the default 512-node tiles only; other tile sizes run the default
+  if constexpr (TN == 512) {
+    constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // select variants need more registers
+    if (var == 6) {
+      constexpr int SMEM = Q * TN * (int)sizeof(T);
+      constexpr int MSM = (200 * 1024) / (SMEM + 512) > 0 ? (200 * 1024) / (SMEM + 512) : 1;
+      constexpr int MB = MSM < M ? MSM : M;
       cudaFuncSetAttribute(k_step_tiles_s<T, TN, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      attr = true;
+      k_step_tiles_s<T, TN, MB><<<nt, BT, SMEM, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                             h->bmask);
+      return;
     }
-    k_step_tiles_s<T, TN, MB><<<nt, BT, SMEM, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
-    return;
+    if (var == 5) {
+      constexpr int MW = sizeof(T) == 4 ? 6 : 3;
+      if (h->n_items)
+        k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items);
+      return;
+    }
+    if (var == 3 || var == 4 || var == 1 || var == 2) {
+      if (var == 3)
+        k_step_tiles<T, TN, 3, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                             h->bmask, h->order, TH);
+      else if (var == 4)
+        k_step_tiles<T, TN, 4, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                             h->bmask, h->order, TH);
+      else if (var == 1)
+        k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                            h->bmask, h->order, TH);
+      else
+        k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                            h->bmask, h->order, TH);
+      return;
+    }
   }
-  if (var == 5) {
-    constexpr int MW = sizeof(T) == 4 ? 6 : 3;
-    if (h->n_items)
-      k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
-          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items);
-    return;
-  }
-  if (var == 3)
-    k_step_tiles<T, TN, 3, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
-  else if (var == 4)
-    k_step_tiles<T, TN, 4, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
-  else if (var == 1)
-    k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
-  else if (var == 2)
-    k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
-  else
-    k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
+  k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask,
+                                                      h->order, TH);
 }
 
 template <typename T, int TN>

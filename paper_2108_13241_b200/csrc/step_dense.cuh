@@ -1,0 +1,287 @@
+// Dense step kernels: the fused pull gather / bounce-back / Zou-He / BGK /
+// store (kernel.py:72-141) for AB and A-A, plus the z-slab halo kernels.
+// Part of liblbm19 (included once, in order, by lbm19.cu).
+#pragma once
+
+// ------------------------------------------------------------------ steps
+// Solid lanes complete the 32-B sectors of their non-solid neighbours with
+// zeros (the values they already hold), so every store is a full sector.
+template <typename T>
+__device__ __forceinline__ bool sector_needs_zero(bool nonsolid) {
+  constexpr int SEC = 32 / (int)sizeof(T);
+  const unsigned act = __ballot_sync(0xffffffffu, nonsolid);
+  const int lane = threadIdx.x & 31;
+  const unsigned grp = ((1u << SEC) - 1u) << (lane & ~(SEC - 1));
+  return (act & grp) != 0u;
+}
+
+// z-slab halo, fused into the step: the outgoing populations of the two
+// boundary planes (c_z = -1 from z = 0, c_z = +1 from z = nz - 1) are stored
+// straight into the neighbouring slab's ghost plane (peer memory over
+// NVLink / IPC), next to the node-local store.  Null pointers: no neighbour.
+__host__ __device__ constexpr int kZm(int j) { return 10 + 2 * j; }  // c_z = -1: 10 12 14 16 18
+__host__ __device__ constexpr int kZp(int j) { return 9 + 2 * j; }   // c_z = +1: 9 11 13 15 17
+template <typename T>
+struct Halo {
+  T* lo[5];  // lower neighbour's upper ghost plane, directions kZm
+  T* hi[5];  // upper neighbour's lower ghost plane, directions kZp
+};
+
+__global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int need_hi,
+                            unsigned long long target, int* err) {
+  const long long t0 = clock64();
+  const volatile unsigned long long* vs = sync;
+  while ((need_lo && vs[0] < target) || (need_hi && vs[1] < target)) {
+    __nanosleep(200);
+    if (clock64() - t0 > 60LL * 2000000000LL) {  // ~1 min at 2 GHz: a neighbour is gone
+      atomicOr(err, 1);
+      return;
+    }
+  }
+  __threadfence_system();
+}
+
+__global__ void k_halo_signal(unsigned long long* lo_slot, unsigned long long* hi_slot,
+                              unsigned long long value) {
+  __threadfence_system();
+  if (lo_slot) *(volatile unsigned long long*)lo_slot = value;
+  if (hi_slot) *(volatile unsigned long long*)hi_slot = value;
+  __threadfence_system();
+}
+
+// initial ghost fill (after initialize / set_pdf): boundary planes of `pre`
+template <typename T>
+__global__ void k_halo_push(const T* __restrict__ pre, Halo<T> H, Geo g) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (x >= g.nxp) return;
+  const int row = y * g.nxp + x;
+  const int s0 = (int)g.plane + row, s1 = g.nz * (int)g.plane + row;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (H.lo[0]) H.lo[j][row] = pre[(long long)kZm(j) * g.ps + s0];
+    if (H.hi[0]) H.hi[j][row] = pre[(long long)kZp(j) * g.ps + s1];
+  }
+  __threadfence_system();
+}
+
+// 19 direction planes of one buffer, resolved on the host once per launch, so
+// every access is a 32-bit slot offset from a per-direction base pointer
+template <typename T>
+struct Planes {
+  const T* pre[Q];
+  T* post[Q];
+};
+
+template <typename T>
+__device__ __forceinline__ void bc_collide(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
+                                           const T* __restrict__ bcr, T om) {
+  const uint32_t t = flag_type(w);
+  if (t == VELOCITY_BC) {
+    const uint32_t b = flag_bc(w);
+    zou_he_velocity19<T>(f, flag_orient(w), bcv[3 * b], bcv[3 * b + 1], bcv[3 * b + 2]);
+  } else if (t == PRESSURE_BC) {
+    zou_he_pressure19<T>(f, flag_orient(w), bcr[flag_bc(w)]);
+  }
+  T rho, vx, vy, vz;
+  moments19(f, rho, vx, vy, vz);
+  collide19(f, rho, vx, vy, vz, om);
+}
+
+template <typename T>
+__device__ __forceinline__ void bc_collide_store(T (&f)[Q], uint32_t w, const T* __restrict__ bcv,
+                                                 const T* __restrict__ bcr, T om,
+                                                 const Planes<T>& P, unsigned s) {
+  bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) P.post[i][s] = f[i];
+}
+
+// Link-wise bounce-back fix-up: every f_i was loaded speculatively from the
+// upstream slot (always a valid address); where the mask bit of opp(i) is
+// clear the node reflects its own f_opp(i) instead (reference kernel.py:84-116).
+template <typename T>
+__device__ __forceinline__ void bounce_back_fixup(T (&f)[Q], uint32_t miss, const Planes<T>& P, unsigned s) {
+  if (miss) {
+#pragma unroll
+    for (int i = 1; i < Q; ++i)
+      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(P.pre[opp(i)] + s);
+  }
+}
+
+// Gather of the 18 moving populations.  MODE 0: speculative pull of every
+// upstream slot, then the fix-up for masked links.  MODE 1: warps whose live
+// nodes all have full masks pull unconditionally, the others select per link
+// so no byte is fetched for a masked link.
+template <typename T, int MODE, typename Up>
+__device__ __forceinline__ void gather(T (&f)[Q], uint32_t miss, bool fast, const Planes<T>& P, unsigned s,
+                                       Up up) {
+  if (MODE == 0 || fast) {
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = __ldg(P.pre[i] + up(i));
+    if (MODE == 0) bounce_back_fixup(f, miss, P, s);
+  } else {
+#pragma unroll
+    for (int i = 1; i < Q; ++i)
+      f[i] = ((miss >> (opp(i) - 1)) & 1u) ? __ldg(P.pre[opp(i)] + s) : __ldg(P.pre[i] + up(i));
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void zero_fill(const Planes<T>& P, unsigned s) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) P.post[i][s] = (T)0;
+}
+
+// dense: offsets from slot s to the upstream node x - c_i, per axis (wrap on
+// periodic axes; on closed axes the edge offset is 0 and the link is masked,
+// so the speculative address stays valid)
+struct UpOffsets {
+  unsigned xm, xp, ym, yp, zm, zp;
+  __device__ __forceinline__ UpOffsets(const Geo& g, int x, int y, int z) {
+    xm = x == 0 ? (g.px ? g.nx - 1 : 0) : -1;
+    xp = x == g.nx - 1 ? (g.px ? -(g.nx - 1) : 0) : 1;
+    ym = y == 0 ? (g.py ? (unsigned)(g.ny - 1) * g.nxp : 0u) : (unsigned)-g.nxp;
+    yp = y == g.ny - 1 ? (g.py ? (unsigned)-((g.ny - 1) * g.nxp) : 0u) : (unsigned)g.nxp;
+    const unsigned pl = (unsigned)g.plane;
+    zm = (z == 0 && g.pzw) ? (unsigned)(g.nz - 1) * pl : 0u - pl;
+    zp = (z == g.nz - 1 && g.pzw) ? 0u - (unsigned)(g.nz - 1) * pl : pl;
+  }
+  // slot of x - c_i
+  __device__ __forceinline__ unsigned up(unsigned s, int i) const {
+    return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0u)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0u)) +
+           (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0u));
+  }
+};
+
+template <typename T, int MODE, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, const uint32_t* __restrict__ flags,
+                                                   const uint32_t* __restrict__ ubits,
+                                                   const T* __restrict__ bcv,
+                                                   const T* __restrict__ bcr, Geo g, T om,
+                                                   const Halo<T> H) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
+  // 32-bit unsigned slot arithmetic (slabs up to 2^32 slots; negative
+  // offsets wrap modulo 2^32 and land on the right slot)
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
+  const unsigned s = fi + (unsigned)g.plane;
+  const uint32_t ub = __ldg(ubits + (fi >> 10));
+  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  const bool live = flag_type(w) != SOLID;
+  const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+  const uint32_t miss = ~w & kMaskBits;
+  // warps whose live nodes all have full masks pull unconditionally; the
+  // rest select per link, so no byte is fetched for a masked link
+  const bool fast = MODE == 1 && __all_sync(0xffffffffu, !live || miss == 0u);
+  if (!live) {
+    if (zfill) zero_fill(P, s);
+    return;
+  }
+  // offsets to the upstream node x - c_i along each axis (wrap on periodic
+  // axes; on closed axes the edge offset is 0 and the link is masked)
+  const UpOffsets o(g, x, y, z);
+  auto up = [&](int i) { return o.up(s, i); };
+  T f[Q];
+  f[0] = __ldg(P.pre[0] + s);
+  gather<T, MODE>(f, miss, fast, P, s, up);
+  bc_collide_store<T>(f, w, bcv, bcr, om, P, s);
+  if ((z == 0 && H.lo[0]) || (z == g.nz - 1 && H.hi[0])) {
+    const int row = y * g.nxp + x;
+    if (z == 0 && H.lo[0]) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) H.lo[j][row] = f[kZm(j)];
+    }
+    if (z == g.nz - 1 && H.hi[0]) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) H.hi[j][row] = f[kZp(j)];
+    }
+    __threadfence_system();
+  }
+}
+
+// A-A in place (LBM_SCHEME_AA): one buffer F, two alternating kernels, each
+// node reading and writing only locations no other node touches in the same
+// launch, so no second buffer is needed.  Per reference step (pull gather of
+// the previous post-collision values, then collide; kernel.py:72-141):
+//   NB = 1 (state phase 0 -> 1), F[opp(i)][x] holds pre_i(x):
+//      f_i = F[opp(i)][x - c_i]  if link opp(i) of x is present (pre_i(x - c_i))
+//          = F[i][x]             otherwise (bounce-back: pre_opp(i)(x))
+//      store f*_i to F[i][x + c_i] if link i is present, else F[opp(i)][x]
+//   NB = 0 (phase 1 -> 0): f_i = F[i][x]; store f*_i to F[opp(i)][x]
+// F[i][x + c_i] is read (as f_opp(i)) and written by node x alone, so the
+// update is race-free; the arithmetic is the AB kernel's, bit for bit.
+template <typename T>
+struct Planes1 {
+  T* f[Q];
+};
+
+// AA loads may take the read-only (non-coherent) path: every location is
+// read and then written by one thread only, so no cached copy can be stale
+template <typename T>
+__device__ __forceinline__ T LDA(const T* p) {
+  return __ldg(p);
+}
+
+// hides a value from the optimiser: the neighbour step's store addresses are
+// the load addresses of the opposite directions, and letting the compiler
+// keep those 18 addresses live across the collision costs spills; an opaque
+// copy makes it recompute them from a handful of offsets instead
+__device__ __forceinline__ unsigned opaque(unsigned v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ int opaque(int v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+
+template <typename T, int NB, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P, const uint32_t* __restrict__ flags,
+                                                      const uint32_t* __restrict__ ubits,
+                                                      const T* __restrict__ bcv, const T* __restrict__ bcr,
+                                                      Geo g, T om) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y, z = blockIdx.z;
+  if (x >= g.nxp) return;
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
+  const unsigned s = fi + (unsigned)g.plane;
+  const uint32_t ub = __ldg(ubits + (fi >> 10));
+  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  // no zero-fill of solid lanes here (unlike the AB kernel): every sector
+  // this step writes was read by the same step, so it sits in L2 whole and a
+  // partial store needs no DRAM read-for-merge; zero stores from solid lanes
+  // would instead race ahead of the live lanes' loads of the same sectors
+  if (flag_type(w) == SOLID) return;
+  const uint32_t miss = ~w & kMaskBits;
+  T f[Q];
+  f[0] = LDA(P.f[0] + s);
+  if (NB) {
+    const UpOffsets o(g, x, y, z);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));  // speculative, always a valid slot
+    if (miss) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(P.f[i] + s);
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+    // recompute the store addresses from opaque copies (measured: keeping the
+    // 18 load addresses live at 64 registers is no faster)
+    const unsigned s2 = opaque(s);
+    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
+    P.f[0][s2] = f[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      T* dst = ((miss >> (i - 1)) & 1u) ? P.f[opp(i)] + s2 : P.f[i] + o2.up(s2, opp(i));
+      *dst = f[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[i] + s);
+    bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) P.f[opp(i)][s] = f[i];
+  }
+}
