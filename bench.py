@@ -77,18 +77,18 @@ def build_workload(name, rank=0, world=1):
         geom = lb.build_porous_random(512, phi, seed=0, radius_range=(4, 32))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
         desc = (f"C3: D3Q19 random-sphere porous medium 512^3, phi target {phi} "
-                f"(achieved {geom.porosity:.3f}), pointer-tile 8^3, fp32")
+                f"(achieved {geom.porosity:.3f}), pointer-tile, fp32")
         return geom, params, "pointer_tile", desc, 1.008
     if name == "porous512":
         geom = lb.build_porous_random(512, 0.5, seed=0, radius_range=(4, 32))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
-        desc = ("C3: D3Q19 random-sphere porous medium 512^3, phi~0.5, pointer-tile 8^3, "
+        desc = ("C3: D3Q19 random-sphere porous medium 512^3, phi~0.5, pointer-tile, "
                 "pressure 1.016 -> 1.0, fp32")
         return geom, params, "pointer_tile", desc, 1.008
     if name == "vascular1024":
         geom = lb.build_vascular(1024, seed=0, fluid_fraction=0.05)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
-        desc = "C4: D3Q19 vascular tube forest 1024^3, ~5% non-solid, pointer-tile 8^3, fp32"
+        desc = "C4: D3Q19 vascular tube forest 1024^3, ~5% non-solid, pointer-tile, fp32"
         return geom, params, "pointer_tile", desc, 1.0
     if name == "c5":
         geom = lb.build_duct_z(1024, 1024, 2048)
@@ -242,7 +242,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
-    ap.add_argument("--tile", default="8,8,8", help="tile edges x,y,z for tile layouts")
+    ap.add_argument("--tile", default="4,8,16",
+                    help="tile edges x,y,z for tile layouts (4x8x16: measured best of 7 shapes, "
+                         "profiles/sparse_r01.md; the API default is 8x8x8)")
     ap.add_argument("--scheme", default=None, choices=["ab", "aa"],
                     help="PDF storage: two buffers (ab) or one in place (aa)")
     ap.add_argument("--no-cpu", action="store_true")
