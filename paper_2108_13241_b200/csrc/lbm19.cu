@@ -466,6 +466,123 @@ void preload_halo_kernels(const lbm_handle* h) {
 
 }  // namespace
 
+// -------------------------------------------- pipelined host <-> device copies
+// host copy split over threads (also spreads the page faults of fresh
+// destination arrays)
+static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
+  size_t total = 0;
+  for (size_t v : n) total += v;
+  static const int hw = [] {
+    const unsigned c = std::thread::hardware_concurrency();
+    return c == 0 ? 8 : (c > 16 ? 16 : (int)c);
+  }();
+  const int nt = total > (8u << 20) ? hw : 1;
+  auto work = [&](int t) {
+    for (size_t k = 0; k < n.size(); ++k) {
+      const size_t per = (n[k] + nt - 1) / nt, a = per * t, b = a + per < n[k] ? a + per : n[k];
+      if (a < b) memcpy(dst_src[k].first + a, dst_src[k].second + a, b - a);
+    }
+  };
+  if (nt == 1) {
+    work(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
+// Pipelined device -> host readback in z chunks: chunk k's kernel and D2H
+// copy (into pinned staging) overlap the host copy of chunk k-1 out of the
+// other pinned slot.  launch(k, z0, nzc, dev) enqueues the chunk kernel;
+// consume(k, z0, nzc, pinned) copies it into the caller's arrays.
+template <class Launch, class Consume>
+static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch, Consume consume) {
+  const long long pn = (long long)h->g.nx * h->g.ny;
+  const size_t want = 64u << 20;  // per staging slot
+  long long cz = (long long)want / (pn * bytes_per_node);
+  if (cz < 1) cz = 1;
+  if (cz > h->g.nz) cz = h->g.nz;
+  if (cz > 65535) cz = 65535;
+  const size_t slot = (size_t)(cz * pn * bytes_per_node);
+  if (h->pin_bytes < slot) {
+    for (int b = 0; b < 2; ++b) {
+      if (h->pin[b]) cudaFreeHost(h->pin[b]);
+      h->pin[b] = nullptr;
+    }
+    h->pin_bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
+      }
+    h->pin_bytes = slot;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
+  char* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, 2 * slot);
+  if (e != cudaSuccess) return fail(LBM_ENOMEM, "readback staging: %s", cudaGetErrorString(e));
+  const int nz = h->g.nz;
+  const int nchunk = (int)((nz + cz - 1) / cz);
+  for (int k = 0; k <= nchunk && e == cudaSuccess; ++k) {
+    if (k < nchunk) {
+      const int b = k & 1, z0 = (int)(k * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
+      launch(k, z0, nzc, dev + b * slot);
+      e = cudaGetLastError();
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(h->pin[b], dev + b * slot, (size_t)(nzc * pn * bytes_per_node), cudaMemcpyDeviceToHost,
+                            h->stream);
+      if (e == cudaSuccess) e = cudaEventRecord(h->evc[b], h->stream);
+    }
+    if (k > 0 && e == cudaSuccess) {
+      const int b = (k - 1) & 1, z0 = (int)((k - 1) * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
+      e = cudaEventSynchronize(h->evc[b]);
+      if (e == cudaSuccess) consume(k - 1, z0, nzc, (const char*)h->pin[b]);
+    }
+  }
+  cudaStreamSynchronize(h->stream);
+  cudaFree(dev);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "readback: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+// Pipelined host -> device upload through the pinned staging slots: the host
+// copy of chunk k+1 (threads) overlaps the DMA of chunk k.
+static int pipelined_h2d(lbm_handle* h, void* dev, const void* host, size_t bytes) {
+  const size_t slot = 64u << 20;
+  if (bytes < (4u << 20)) {  // small: one plain copy
+    CK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, h->stream));
+    return 0;
+  }
+  if (h->pin_bytes < slot) {
+    for (int b = 0; b < 2; ++b) {
+      if (h->pin[b]) cudaFreeHost(h->pin[b]);
+      h->pin[b] = nullptr;
+    }
+    h->pin_bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
+      }
+    h->pin_bytes = slot;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
+  const size_t n = (bytes + slot - 1) / slot;
+  for (size_t k = 0; k < n; ++k) {
+    const int b = (int)(k & 1);
+    const size_t off = k * slot, len = bytes - off < slot ? bytes - off : slot;
+    CK(cudaEventSynchronize(h->evc[b]));  // slot b's previous DMA (this or an earlier call) is done
+    par_copy({{(char*)h->pin[b], (const char*)host + off}}, {len});
+    CK(cudaMemcpyAsync((char*)dev + off, h->pin[b], len, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(h->evc[b], h->stream));
+  }
+  return 0;
+}
+
 // ================================================================= C-ABI
 extern "C" {
 
@@ -663,9 +780,9 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       (rc = dev_alloc(h, &dbc, N * 4)) || (rc = dev_alloc(h, &derr, 16)))
     goto done;
   pt.mark("alloc temporaries");
-  CK(cudaMemcpyAsync(dtype_, type, N, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(dorient, orient, N, cudaMemcpyHostToDevice, h->stream));
-  CK(cudaMemcpyAsync(dbc, bc_index, N * 4, cudaMemcpyHostToDevice, h->stream));
+  if ((rc = pipelined_h2d(h, dtype_, type, N)) || (rc = pipelined_h2d(h, dorient, orient, N)) ||
+      (rc = pipelined_h2d(h, dbc, bc_index, N * 4)))
+    goto done;
   CK(cudaMemsetAsync(derr, 0, 16, h->stream));
   CK(cudaMemsetAsync(h->uscratch, 0, 4 * sizeof(unsigned long long), h->stream));
   if (ghost_lo) {
@@ -1042,85 +1159,6 @@ int chunk_planes(const lbm_handle* h, long long bytes_per_node) {
   return (int)c;
 }
 
-extern "C++" {
-// host copy split over threads (also spreads the page faults of fresh
-// destination arrays)
-static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
-  size_t total = 0;
-  for (size_t v : n) total += v;
-  const int nt = total > (8u << 20) ? 8 : 1;
-  auto work = [&](int t) {
-    for (size_t k = 0; k < n.size(); ++k) {
-      const size_t per = (n[k] + nt - 1) / nt, a = per * t, b = a + per < n[k] ? a + per : n[k];
-      if (a < b) memcpy(dst_src[k].first + a, dst_src[k].second + a, b - a);
-    }
-  };
-  if (nt == 1) {
-    work(0);
-    return;
-  }
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
-}
-
-// Pipelined device -> host readback in z chunks: chunk k's kernel and D2H
-// copy (into pinned staging) overlap the host copy of chunk k-1 out of the
-// other pinned slot.  launch(k, z0, nzc, dev) enqueues the chunk kernel;
-// consume(k, z0, nzc, pinned) copies it into the caller's arrays.
-template <class Launch, class Consume>
-static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch, Consume consume) {
-  const long long pn = (long long)h->g.nx * h->g.ny;
-  const size_t want = 64u << 20;  // per staging slot
-  long long cz = (long long)want / (pn * bytes_per_node);
-  if (cz < 1) cz = 1;
-  if (cz > h->g.nz) cz = h->g.nz;
-  if (cz > 65535) cz = 65535;
-  const size_t slot = (size_t)(cz * pn * bytes_per_node);
-  if (h->pin_bytes < slot) {
-    for (int b = 0; b < 2; ++b) {
-      if (h->pin[b]) cudaFreeHost(h->pin[b]);
-      h->pin[b] = nullptr;
-    }
-    h->pin_bytes = 0;
-    for (int b = 0; b < 2; ++b)
-      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
-      }
-    h->pin_bytes = slot;
-  }
-  for (int b = 0; b < 2; ++b)
-    if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
-  char* dev = nullptr;
-  cudaError_t e = cudaMalloc(&dev, 2 * slot);
-  if (e != cudaSuccess) return fail(LBM_ENOMEM, "readback staging: %s", cudaGetErrorString(e));
-  const int nz = h->g.nz;
-  const int nchunk = (int)((nz + cz - 1) / cz);
-  for (int k = 0; k <= nchunk && e == cudaSuccess; ++k) {
-    if (k < nchunk) {
-      const int b = k & 1, z0 = (int)(k * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
-      launch(k, z0, nzc, dev + b * slot);
-      e = cudaGetLastError();
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(h->pin[b], dev + b * slot, (size_t)(nzc * pn * bytes_per_node), cudaMemcpyDeviceToHost,
-                            h->stream);
-      if (e == cudaSuccess) e = cudaEventRecord(h->evc[b], h->stream);
-    }
-    if (k > 0 && e == cudaSuccess) {
-      const int b = (k - 1) & 1, z0 = (int)((k - 1) * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
-      e = cudaEventSynchronize(h->evc[b]);
-      if (e == cudaSuccess) consume(k - 1, z0, nzc, (const char*)h->pin[b]);
-    }
-  }
-  cudaStreamSynchronize(h->stream);
-  cudaFree(dev);
-  if (e != cudaSuccess) return fail(LBM_ECUDA, "readback: %s", cudaGetErrorString(e));
-  return 0;
-}
-
-}  // extern "C++"
 
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
