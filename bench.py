@@ -206,7 +206,8 @@ def run_reference_arm(args):
     import paper_2108_13241_b200 as lb
     cores = len(os.sched_getaffinity(0))
     numba.set_num_threads(cores)
-    budget_updates = 2.0e9   # ~1 minute of CPU work for the whole timed run
+    # ~1 minute of CPU work for the whole timed run (LBM_REF_BUDGET: node updates)
+    budget_updates = float(os.environ.get("LBM_REF_BUDGET", "2.0e9"))
     nzs = int(max(1, min(512, round(budget_updates / (args.steps * 512 * 512)))))
     geom = lb.build_channel(512, 512, nzs, lb.VelocityInlet((0.05, 0.0, 0.0)))
     omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25).omega
