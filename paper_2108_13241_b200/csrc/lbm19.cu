@@ -377,6 +377,7 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
   // fast path else per-link select; 2 / 3 the same with a looser register cap
   const int var = h->variant;
   constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
+  constexpr int V4B = 3;  // 128-bit kernel: 3 x 128 threads per SM, up to 168 registers
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   if (g.aa) {
@@ -412,6 +413,16 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
       k_step_dense<T, 0, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
     else if (var == 3)
       k_step_dense<T, 1, D2><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
+    else if (var == 8 && sizeof(T) == 4 && !halo_on(h)) {
+      Planes<float> P4;
+      for (int i = 0; i < Q; ++i) {
+        P4.pre[i] = (const float*)P.pre[i];
+        P4.post[i] = (float*)P.post[i];
+      }
+      const dim3 g4((g.nxp / 4 + 127) / 128, g.ny, g.nz);
+      k_step_dense_v4<V4B><<<g4, 128, 0, h->stream>>>(P4, h->flags, h->ubits, (const float*)bv, (const float*)br, g,
+                                                       (float)om);
+    }
     else
       k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
   } else {

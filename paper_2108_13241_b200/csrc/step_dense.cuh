@@ -201,6 +201,92 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   }
 }
 
+// Dense AB step with 128-bit accesses: four consecutive x-nodes per thread,
+// 19 LDG.128 + 19 STG.128 per quad.  Directions with c_x = 0 load the
+// upstream quad directly; c_x = +-1 load the aligned quad of the upstream row
+// and take the one element that crosses into the neighbouring quad from the
+// adjacent lane (__shfl_up/down), or from memory at warp ends.  Closed-x edge
+// values are masked links and are replaced by the bounce-back fix-up; on a
+// periodic x axis the wrapped elements are reloaded.  fp32 only, no halo.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB)
+k_step_dense_v4(const Planes<float> P, const uint32_t* __restrict__ flags, const uint32_t* __restrict__ ubits,
+                const float* __restrict__ bcv, const float* __restrict__ bcr, Geo g, float om) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int y = blockIdx.y, z = blockIdx.z;
+  const bool act = x0 < g.nxp;
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + (act ? x0 : 0);
+  const unsigned s = fi + (unsigned)g.plane;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if (act) {
+    const uint32_t ub = __ldg(ubits + (fi >> 10));
+    if ((ub >> ((fi >> 5) & 31)) & 1u) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = make_flag(kMaskBits, FLUID, 0, 0);
+    } else {
+      const uint4 fw = __ldg(reinterpret_cast<const uint4*>(flags + fi));
+      w[0] = fw.x, w[1] = fw.y, w[2] = fw.z, w[3] = fw.w;
+    }
+  }
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) any |= flag_type(w[k]) != SOLID;
+  // the other quad of this quad's 32-B sector sits in lane ^ 1
+  const bool partner = __shfl_xor_sync(FULL, (int)any, 1) != 0;
+  const UpOffsets o(g, 0, y, z);
+  float4 v[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const unsigned r = s + (cy(i) == 1 ? o.ym : (cy(i) == -1 ? o.yp : 0u)) + (cz(i) == 1 ? o.zm : (cz(i) == -1 ? o.zp : 0u));
+    const float4 a = __ldg(reinterpret_cast<const float4*>(P.pre[i] + r));
+    if (cx(i) == 0) {
+      v[i] = a;
+    } else if (cx(i) == 1) {  // upstream x - 1
+      float pw = __shfl_up_sync(FULL, a.w, 1);
+      if (lane == 0) pw = (act && x0 > 0) ? __ldg(P.pre[i] + r - 1) : 0.f;
+      if (g.px && x0 == 0 && act) pw = __ldg(P.pre[i] + r + (g.nx - 1));
+      v[i] = make_float4(pw, a.x, a.y, a.z);
+    } else {                 // upstream x + 1
+      float nx_ = __shfl_down_sync(FULL, a.x, 1);
+      if (lane == 31) nx_ = (act && x0 + 4 < g.nxp) ? __ldg(P.pre[i] + r + 4) : 0.f;
+      v[i] = make_float4(a.y, a.z, a.w, nx_);
+      if (g.px && act && x0 <= g.nx - 1 && g.nx - 1 < x0 + 4) {
+        const float wv = __ldg(P.pre[i] + r - x0);  // x = 0 of the upstream row
+        const int k = g.nx - 1 - x0;
+        if (k == 0) v[i].x = wv; else if (k == 1) v[i].y = wv; else if (k == 2) v[i].z = wv; else v[i].w = wv;
+      }
+    }
+  }
+  if (!act || !(any || (partner && g.zero_fill))) return;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float f[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = k == 0 ? v[i].x : (k == 1 ? v[i].y : (k == 2 ? v[i].z : v[i].w));
+    const uint32_t wk = w[k];
+    if (flag_type(wk) != SOLID) {
+      const uint32_t miss = ~wk & kMaskBits;
+      if (miss) {
+#pragma unroll
+        for (int i = 1; i < Q; ++i)
+          if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(P.pre[opp(i)] + s + k);
+      }
+      bc_collide<float>(f, wk, bcv, bcr, om);
+    } else {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) f[i] = 0.f;  // solid: storage stays 0 (full-sector stores)
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      if (k == 0) v[i].x = f[i]; else if (k == 1) v[i].y = f[i]; else if (k == 2) v[i].z = f[i]; else v[i].w = f[i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) *reinterpret_cast<float4*>(P.post[i] + s) = v[i];
+}
+
 // A-A in place (LBM_SCHEME_AA): one buffer F, two alternating kernels, each
 // node reading and writing only locations no other node touches in the same
 // launch, so no second buffer is needed.  Per reference step (pull gather of
