@@ -389,3 +389,19 @@ def test_square_duct_profile_matches_analytic():
     assert err < 0.03, err
     # mass flux through the section equals the inflow (incompressible, steady)
     assert abs(sim_p.sum() - 0.02 * n * n) / (0.02 * n * n) < 0.05
+
+
+def test_porosity_sweep_reports(tmp_path):
+    """Reference porosity_sweep (metrics.py:159-203) over the device path:
+    a dense reference per layout plus one report per cell, eta_P filled,
+    regular placements below 0.3 skipped; CSV with the documented columns."""
+    cfg = lb.SweepConfig(n=64, warmup_steps=3, timed_steps=10, radius_range=(3, 8))
+    reps = lb.porosity_sweep(["dense", "pointer_tile"], [0.2, 0.5], config=cfg)
+    assert len(reps) == 2 * (1 + 1 + 2)
+    for r in reps:
+        assert r.p_lups > 0 and r.eta_p is not None and r.consistent()
+    assert [r.placement for r in reps[:4]] == ["dense", "regular", "random", "random"]
+    path = tmp_path / "sweep.csv"
+    lb.write_report_csv(reps, path, config_hash="abc")
+    lines = path.read_text().splitlines()
+    assert lines[0] == "# config_hash abc" and len(lines) == 2 + len(reps)

@@ -163,3 +163,19 @@ def test_perf_report_arithmetic():
     assert r.b_node_bytes == 152
     assert r.p_lups == 1000.0
     assert r.consistent()
+
+
+def test_build_porous_regular_hits_porosity():
+    """3-D analogue of the reference's regular array (geometry.py:315-370):
+    bisection on the sphere radius reaches the target within 0.02; below 0.3
+    is refused like the reference."""
+    for phi in (0.3, 0.45, 0.6, 0.9, 1.0):
+        g = lb.build_porous_regular(64, phi)
+        assert abs(g.porosity - phi) <= 0.02 + 1e-12, (phi, g.porosity)
+        t = g.descriptors.type_tag
+        # walls win: no solid node on the domain faces, solids wrapped in walls
+        assert not (t[:, :, 0] == lb.NodeType.SOLID).any()
+    with pytest.raises(lb.GeometryError):
+        lb.build_porous_regular(64, 0.2)
+    with pytest.raises(lb.GeometryError):
+        lb.build_porous_regular(32, 0.5)
