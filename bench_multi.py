@@ -35,7 +35,19 @@ def run_multi(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dev = "cuda"
     workload = args.workload or "channel512"
-    if workload == "duct":
+    scaling = "weak"
+    if workload == "c5":
+        # strong scaling of the whole C5 domain: 2048 / N planes per GPU (AB
+        # fits from N = 2; N = 1 is bench.py --workload c5 with the A-A scheme)
+        if 2048 % world:
+            raise SystemExit(f"c5 needs N dividing 2048, got {world}")
+        geom, spec = duct_slab(1024, 1024, 2048 // world, rank, world)
+        params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
+        desc = (f"C5 strong scaling: D3Q19 duct 1024x1024x2048 along z in {world} z-slabs of "
+                f"1024x1024x{2048 // world}, velocity inlet / pressure outlet, fp32")
+        periodic = False
+        scaling = "strong"
+    elif workload == "duct":
         geom, spec = duct_slab(1024, 1024, 256, rank, world)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
         desc = (f"C5: D3Q19 duct 1024x1024x{256 * world} along z, z-slabs of 1024x1024x256 per "
@@ -88,7 +100,7 @@ def run_multi(args, rank, world, local):
         line = {
             "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": desc, "layout": "dense", "nodes_per_gpu": int(per_gpu_nodes),
                        "l2": "state per GPU >> 126 MB L2 (no flush needed)",
