@@ -349,6 +349,14 @@ def main():
         del fields
         s2.close()
 
+    # second calibration: this library's own device copy kernel on a 4 GiB
+    # block (the reference's copy micro-benchmark, dense pattern)
+    copy_gbs = None
+    try:
+        copy_gbs = lb.copy_bandwidth_bench("dense", 4 << 30, repetitions=20, warmup=3, device=local) / 1e9
+    except Exception:
+        copy_gbs = None
+
     cpu = None
     if not args.no_cpu:
         try:
@@ -373,6 +381,8 @@ def main():
                      "alg_bytes_per_launch": alg_bytes,
                      "alg_bytes_per_node": alg_bytes / nons,
                      "meta_bytes_per_launch": int(st.meta_bytes_per_step),
+                     "copy_gbs": copy_gbs,
+                     "frac_of_copy": (achieved / copy_gbs) if copy_gbs else None,
                      "frac_152B": nons * 152 / (per_launch_ms / 1e3) / 1e9 / peak,
                      "frac_156B": nons * 156 / (per_launch_ms / 1e3) / 1e9 / peak},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,

@@ -112,6 +112,14 @@ int lbm_abi_version(void);
 int lbm_device_count(int* n);
 
 int lbm_create(const lbm_desc* desc, lbm_t** out);
+/* Copy-bandwidth micro-benchmark (reference layouts.copy_bandwidth_bench,
+ * layouts.py:473-510) on the device: a flat f64 block of block_bytes copied
+ * with the access pattern of `layout` (dense: contiguous 128-bit; bitmask_node:
+ * masked; tile: 256-node chunks; pointer_tile: chunks through a base table),
+ * warmup untimed + repetitions timed (CUDA events); *bytes_per_s = 2 * bytes *
+ * repetitions / elapsed.  The destination is verified (LBM_ESTATE if not). */
+int lbm_copy_bandwidth(int32_t device, int32_t layout, int64_t block_bytes, int32_t repetitions,
+                       int32_t warmup, double* bytes_per_s);
 void lbm_destroy(lbm_t* h);
 
 /* Node descriptors of this handle's nodes, canonical (nz, ny, nx) arrays.

@@ -53,6 +53,7 @@ SIGNATURES = [
     ("lbm_abi_version", C.c_int, []),
     ("lbm_device_count", C.c_int, [C.POINTER(C.c_int)]),
     ("lbm_create", C.c_int, [C.POINTER(LbmDesc), C.POINTER(P)]),
+    ("lbm_copy_bandwidth", C.c_int, [I32, I32, I64, I32, I32, PD]),
     ("lbm_destroy", None, [P]),
     ("lbm_set_geometry", C.c_int, [P, P, P, P, P, P, P, P, P, I32]),
     ("lbm_init_equilibrium", C.c_int, [P, P, P, P, P, D, D, D, D]),

@@ -606,6 +606,78 @@ int lbm_device_count(int* n) {
   return 0;
 }
 
+int lbm_copy_bandwidth(int32_t device, int32_t layout, int64_t block_bytes, int32_t repetitions, int32_t warmup,
+                       double* bytes_per_s) {
+  if (!bytes_per_s) return fail(LBM_EINVAL, "bytes_per_s is NULL");
+  if (block_bytes < 64 * 1024) return fail(LBM_EINVAL, "block_bytes must be at least 64 KiB, got %lld", (long long)block_bytes);
+  if (repetitions < 1 || warmup < 0) return fail(LBM_EINVAL, "need repetitions >= 1 and warmup >= 0");
+  if (layout < 0 || layout > LBM_LAYOUT_POINTER_TILE) return fail(LBM_EINVAL, "unknown layout %d", layout);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(LBM_EINVAL, "device %d not present", device);
+  DeviceGuard dg(device);
+  constexpr int kChunk = 256;  // the reference's TILE_NODES (16 x 16)
+  const long long n = block_bytes / 8 / kChunk * kChunk;
+  double *src = nullptr, *dst = nullptr;
+  uint8_t* mask = nullptr;
+  long long* base = nullptr;
+  unsigned long long* bad = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = 0;
+  cudaError_t e = cudaMalloc(&src, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dst, n * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&bad, 8);
+  if (e == cudaSuccess && layout == LBM_LAYOUT_BITMASK_NODE) e = cudaMalloc(&mask, n);
+  if (e == cudaSuccess && layout == LBM_LAYOUT_POINTER_TILE) e = cudaMalloc(&base, n / kChunk * 8);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    rc = fail(LBM_ENOMEM, "copy bench: cannot allocate 2 x %lld byte blocks", n * 8);
+  } else {
+    k_iota<<<1184, 256>>>(src, n);
+    cudaMemset(dst, 0, n * 8);
+    cudaMemset(bad, 0, 8);
+    if (mask) cudaMemset(mask, 1, n);
+    if (base) {
+      std::vector<long long> hb(n / kChunk);
+      for (size_t c = 0; c < hb.size(); ++c) hb[c] = (long long)c * kChunk;
+      cudaMemcpy(base, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice);
+    }
+    auto run = [&]() {
+      if (layout == LBM_LAYOUT_DENSE)
+        k_copy_dense<<<(unsigned)((n / 2 + 1023) / 1024), 256>>>((const double2*)src, (double2*)dst, n / 2);
+      else if (layout == LBM_LAYOUT_BITMASK_NODE)
+        k_copy_masked<<<148 * 8, 256>>>(src, dst, mask, n);
+      else
+        k_copy_chunked<<<(unsigned)(n / kChunk), kChunk, 0>>>(src, dst, base, kChunk);
+    };
+    for (int k = 0; k < warmup; ++k) run();
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int k = 0; k < repetitions; ++k) run();
+    cudaEventRecord(e1);
+    e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long nbad = 0;
+    if (e == cudaSuccess) {
+      k_count_diff<<<1184, 256>>>(src, dst, n, bad);
+      e = cudaMemcpy(&nbad, bad, 8, cudaMemcpyDeviceToHost);
+    }
+    if (e != cudaSuccess)
+      rc = fail(LBM_ECUDA, "copy bench: %s", cudaGetErrorString(e));
+    else if (nbad)
+      rc = fail(LBM_ESTATE, "copy benchmark produced a corrupted destination (%llu elements)", nbad);
+    else
+      *bytes_per_s = 2.0 * (double)n * 8.0 * repetitions / (ms / 1e3);
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  for (void* p : {(void*)src, (void*)dst, (void*)mask, (void*)base, (void*)bad})
+    if (p) cudaFree(p);
+  return rc;
+}
+
 int lbm_create(const lbm_desc* desc, lbm_t** out) {
   if (!desc || !out) return fail(LBM_EINVAL, "desc/out is NULL");
   const lbm_desc& d = *desc;

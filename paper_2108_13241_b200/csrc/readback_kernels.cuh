@@ -217,3 +217,47 @@ __global__ void k_mass_final(const double* __restrict__ partial, int n, double* 
   }
   if (threadIdx.x == 0) *out = sh[0];
 }
+
+// ------------------------------------------------ copy-bandwidth micro-bench
+// Device versions of the reference's layout copy kernels (layouts.py:443-470):
+// the achievable HBM copy bandwidth for each access pattern, used as the
+// roofline calibration next to MEASURED_PEAKS.json.
+// one pass, no grid-stride loop: each CTA copies 4 x blockDim 16-B elements,
+// four independent loads in flight per thread (streaming cache hints)
+__global__ void k_copy_dense(const double2* __restrict__ src, double2* __restrict__ dst, long long n2) {
+  const long long i0 = (long long)blockIdx.x * blockDim.x * 4 + threadIdx.x;
+  double2 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long i = i0 + (long long)k * blockDim.x;
+    if (i < n2) v[k] = __ldcs(src + i);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const long long i = i0 + (long long)k * blockDim.x;
+    if (i < n2) __stcs(dst + i, v[k]);
+  }
+}
+__global__ void k_copy_masked(const double* __restrict__ src, double* __restrict__ dst,
+                              const uint8_t* __restrict__ mask, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (__ldg(mask + i)) dst[i] = __ldg(src + i);
+}
+// one CTA per chunk of `chunk` nodes; base offsets from a table (pointer tiles) or implicit
+__global__ void k_copy_chunked(const double* __restrict__ src, double* __restrict__ dst,
+                               const long long* __restrict__ base, int chunk) {
+  const long long b = base ? __ldg(base + blockIdx.x) : (long long)blockIdx.x * chunk;
+  for (int j = threadIdx.x; j < chunk; j += blockDim.x) dst[b + j] = __ldg(src + b + j);
+}
+__global__ void k_count_diff(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                             unsigned long long* bad) {
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    c += a[i] != b[i];
+  if (c) atomicAdd(bad, c);
+}
+__global__ void k_iota(double* __restrict__ a, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    a[i] = (double)i;
+}
+

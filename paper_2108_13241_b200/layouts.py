@@ -187,3 +187,38 @@ class NodeDescriptorField:
                 and np.array_equal(self.bc_index, other.bc_index)
                 and np.array_equal(self.orientation, other.orientation)
                 and self.periodic == other.periodic)
+
+
+# ---------------------------------------------------------------------------
+# copy micro-benchmark (reference layouts.py:439-524), on the device
+
+
+def copy_bandwidth_bench(layout, block_bytes, repetitions=100, warmup=5, device=0):
+    """Achieved device copy bandwidth (bytes/s, read + write) for one
+    layout's access pattern: a flat f64 block of `block_bytes` copied
+    `repetitions` times after `warmup` untimed copies (CUDA events), the
+    destination verified (reference layouts.py:473-510)."""
+    import ctypes as C
+
+    from . import _lib
+    layout = LayoutKind.parse(layout) if not isinstance(layout, LayoutKind) else layout
+    out = C.c_double(0.0)
+    lib = _lib.load()
+    _lib.check(lib.lbm_copy_bandwidth(int(device), _lib.LAYOUT_CODES[layout.value], int(block_bytes),
+                                      int(repetitions), int(warmup), C.byref(out)), "copy_bandwidth_bench")
+    return float(out.value)
+
+
+def copy_bandwidth_survey(block_bytes, repetitions=20, device=0):
+    """Bandwidth per layout plus a logged (never asserted) ordering check
+    (reference layouts.py:513-524)."""
+    import logging
+    results = {k: copy_bandwidth_bench(k, block_bytes, repetitions, device=device) for k in LayoutKind}
+    dense, bitmask, pointer = (results[LayoutKind.DENSE], results[LayoutKind.BITMASK_NODE],
+                               results[LayoutKind.POINTER_TILE])
+    if not dense >= bitmask >= pointer:
+        logging.getLogger(__name__).info(
+            "copy-bandwidth ordering dense >= bitmask >= pointer not observed: %s",
+            {k.value: f"{v / 1e9:.2f} GB/s" for k, v in results.items()})
+    return results
+

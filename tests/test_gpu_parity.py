@@ -405,3 +405,12 @@ def test_porosity_sweep_reports(tmp_path):
     lb.write_report_csv(reps, path, config_hash="abc")
     lines = path.read_text().splitlines()
     assert lines[0] == "# config_hash abc" and len(lines) == 2 + len(reps)
+
+
+def test_copy_bandwidth_survey_on_device():
+    """Reference copy micro-benchmark (layouts.py:473-524) on the device:
+    every layout pattern copies a verified block; dense is a real HBM rate."""
+    res = lb.copy_bandwidth_survey(256 << 20, repetitions=5)
+    assert set(res) == set(lb.LayoutKind)
+    assert all(v > 1e11 for v in res.values())
+    assert res[lb.LayoutKind.DENSE] > 2e12

@@ -179,3 +179,10 @@ def test_build_porous_regular_hits_porosity():
         lb.build_porous_regular(64, 0.2)
     with pytest.raises(lb.GeometryError):
         lb.build_porous_regular(32, 0.5)
+
+
+def test_copy_bandwidth_argument_errors_without_device():
+    with pytest.raises(ValueError):
+        lb.copy_bandwidth_bench("dense", 1024)          # below 64 KiB (reference bound)
+    with pytest.raises(ValueError):
+        lb.copy_bandwidth_bench("dense", 1 << 20, repetitions=0)
