@@ -414,3 +414,36 @@ def test_copy_bandwidth_survey_on_device():
     assert set(res) == set(lb.LayoutKind)
     assert all(v > 1e11 for v in res.values())
     assert res[lb.LayoutKind.DENSE] > 2e12
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("scheme", ["ab", "aa"])
+def test_all_solid_domain_is_a_no_op(layout, scheme):
+    """Empty input: no non-solid node, no kept tile; stepping, readbacks,
+    mass and the finite check still work and report zeros."""
+    types = np.zeros((6, 9, 13), dtype=np.uint8)
+    sim = lb.Simulation(lb.from_arrays("solid", types), params_for(1.1), layout=layout,
+                        scalar=np.float32, scheme=scheme)
+    sim.initialize(1.0)
+    sim.step(5)
+    assert sim.active_node_count == 0
+    assert not sim.canonical_state().any()
+    assert all(not a.any() for a in sim.macroscopic_fields())
+    assert sim.total_mass() == 0.0
+    sim.check_finite()
+
+
+def test_boundary_table_limit_and_bad_descriptors():
+    """At most 255 boundary-table entries fit the flag word (bc index bits
+    24-31); out-of-range types / missing bc indices are rejected."""
+    types = np.full((4, 8, 8), lb.NodeType.FLUID, dtype=np.uint8)
+    big = lb.BoundaryValueTable()
+    for k in range(256):
+        big.add_velocity(0.001 * k, 0.0, 0.0)
+    geom = lb.from_arrays("box", types, big)
+    with pytest.raises(ValueError, match="255"):
+        lb.Simulation(geom, params_for(1.1), scalar=np.float32)
+    g2 = lb.from_arrays("box", types)
+    g2.descriptors.type_tag[1, 2, 3] = 7          # corrupt after validation
+    with pytest.raises(ValueError, match="out of range"):
+        lb.Simulation(g2, params_for(1.1), scalar=np.float32)

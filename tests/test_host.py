@@ -186,3 +186,33 @@ def test_copy_bandwidth_argument_errors_without_device():
         lb.copy_bandwidth_bench("dense", 1024)          # below 64 KiB (reference bound)
     with pytest.raises(ValueError):
         lb.copy_bandwidth_bench("dense", 1 << 20, repetitions=0)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(layout="pointer_tile", tile=(3, 8, 8)), "powers of two"),
+    (dict(layout="pointer_tile", tile=(2, 2, 2)), "32..512"),
+    (dict(layout="tile", tile=(16, 16, 16)), "32..512"),
+    (dict(scheme="aa", slab=True), "single-slab"),
+])
+def test_create_argument_validation_without_device(kw, msg):
+    """lbm_create validates the descriptor before it touches a device, so the
+    reference's ValueError contract (kernel.py:201-206, layouts.py:370-379)
+    holds on any host."""
+    from paper_2108_13241_b200.distributed import slab_geometry
+    geom = lb.build_channel(16, 8, 8, lb.VelocityInlet((0.01, 0.0, 0.0)))
+    params = lb.FlowParams.from_viscosity(U=0.01, L=7, nu=0.1)
+    kw = dict(kw)
+    if kw.pop("slab", False):
+        geom, kw["slab"] = slab_geometry(geom, 0, 4)
+    with pytest.raises(ValueError, match=msg):
+        lb.Simulation(geom, params, scalar=np.float32, **kw)
+
+
+def test_periodic_axis_must_divide_tile_without_device():
+    types = np.full((8, 8, 12), lb.NodeType.FLUID, dtype=np.uint8)
+    geom = lb.from_arrays("box", types, periodic=(True, False, False))
+    params = lb.FlowParams.from_viscosity(U=0.01, L=7, nu=0.1)
+    with pytest.raises(ValueError, match="periodic axis"):
+        lb.Simulation(geom, params, layout="pointer_tile", tile=(8, 4, 4))
+    with pytest.raises(ValueError, match="scalar"):
+        lb.Simulation(geom, params, layout="dense", scalar=np.float16)
