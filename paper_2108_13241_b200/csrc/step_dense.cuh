@@ -168,7 +168,24 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
   const unsigned s = fi + (unsigned)g.plane;
   const uint32_t ub = __ldg(ubits + (fi >> 10));
-  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  const bool uni = (ub >> ((fi >> 5) & 31)) & 1u;  // warp-uniform: one chunk = one warp
+  if (uni && !((z == 0 && H.lo[0]) || (z == g.nz - 1 && H.hi[0]))) {
+    // uniform chunk (all FLUID / wall, full masks) off the halo planes: no
+    // flag word, no bounce-back, no closure, no zero fill -- the same
+    // arithmetic as the general path below, without its control flow
+    const UpOffsets o(g, x, y, z);
+    T f[Q];
+    f[0] = __ldg(P.pre[0] + s);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = __ldg(P.pre[i] + o.up(s, i));
+    T rho, vx, vy, vz;
+    moments19(f, rho, vx, vy, vz);
+    collide19(f, rho, vx, vy, vz, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) P.post[i][s] = f[i];
+    return;
+  }
+  const uint32_t w = uni ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
   const bool live = flag_type(w) != SOLID;
   const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
   const uint32_t miss = ~w & kMaskBits;
