@@ -370,6 +370,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "layout": layout, "scheme": scheme,
                    "tile": list(tile) if layout in ("tile", "pointer_tile") else None,
+                   "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile")
+                                   if layout in ("tile", "pointer_tile") else None),
                    "nodes": int(st.n_nodes),
                    "non_solid_nodes": int(nons), "tiles": int(st.n_tiles),
                    "l2": "state 2x19 planes >> 126 MB L2 (no flush needed)",

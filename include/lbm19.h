@@ -103,6 +103,7 @@ typedef struct lbm_stats {
   int32_t parity;           /* AB: index of the pre buffer; AA: step phase (step_count mod 2) */
   int32_t initialized;
   int32_t scheme;           /* LBM_SCHEME_* */
+  int32_t tile_work_list;   /* 1: tile steps run one warp per live-brick group (sparse tiles) */
 } lbm_stats;
 
 typedef struct lbm_handle lbm_t;

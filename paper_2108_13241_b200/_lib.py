@@ -38,7 +38,7 @@ class LbmStats(C.Structure):
                 ("device_bytes", C.c_int64), ("launches_total", C.c_int64),
                 ("last_step_ms", C.c_double), ("meta_bytes_per_step", C.c_int64),
                 ("parity", C.c_int32),
-                ("initialized", C.c_int32), ("scheme", C.c_int32)]
+                ("initialized", C.c_int32), ("scheme", C.c_int32), ("tile_work_list", C.c_int32)]
 
 
 P = C.c_void_p
