@@ -65,41 +65,41 @@ def build_workload(name, rank=0, world=1):
         geom = lb.build_channel(512, 512, 512, lb.VelocityInlet((0.05, 0.0, 0.0)))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25)
         desc = ("C2: D3Q19 dense channel 512^3, velocity inlet u=0.05 (x=0), pressure "
-                "outlet rho=1 (x=511), bounce-back y walls, periodic z, nu=0.25, fp32")
+                "outlet rho=1 (x=511), bounce-back y walls, periodic z, nu=0.25")
         return geom, params, "dense", desc, 1.0
     if name == "cavity64":
         geom = lb.build_cavity(64, 64, 64, 0.1)
         params = lb.FlowParams.from_reynolds(U=0.1, L=63, Re=100)
-        desc = "C1: D3Q19 lid-driven cavity 64^3, Re 100, fp32 (L2-resident; parity config)"
+        desc = "C1: D3Q19 lid-driven cavity 64^3, Re 100(L2-resident; parity config)"
         return geom, params, "dense", desc, 1.0
     if name.startswith("porous512@"):
         phi = float(name.split("@")[1])
         geom = lb.build_porous_random(512, phi, seed=0, radius_range=(4, 32))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
         desc = (f"C3: D3Q19 random-sphere porous medium 512^3, phi target {phi} "
-                f"(achieved {geom.porosity:.3f}), pointer-tile, fp32")
+                f"(achieved {geom.porosity:.3f}), pointer-tile")
         return geom, params, "pointer_tile", desc, 1.008
     if name == "porous512":
         geom = lb.build_porous_random(512, 0.5, seed=0, radius_range=(4, 32))
         params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5)
         desc = ("C3: D3Q19 random-sphere porous medium 512^3, phi~0.5, pointer-tile, "
-                "pressure 1.016 -> 1.0, fp32")
+                "pressure 1.016 -> 1.0")
         return geom, params, "pointer_tile", desc, 1.008
     if name == "vascular1024":
         geom = lb.build_vascular(1024, seed=0, fluid_fraction=0.05)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
-        desc = "C4: D3Q19 vascular tube forest 1024^3, ~5% non-solid, pointer-tile, fp32"
+        desc = "C4: D3Q19 vascular tube forest 1024^3, ~5% non-solid, pointer-tile"
         return geom, params, "pointer_tile", desc, 1.0
     if name == "c5":
         geom = lb.build_duct_z(1024, 1024, 2048)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
         desc = ("C5 whole domain on one GPU: D3Q19 duct 1024x1024x2048 along z, velocity inlet "
-                "z=0, pressure outlet z=2047, bounce-back x/y faces, fp32 (needs the AA scheme)")
+                "z=0, pressure outlet z=2047, bounce-back x/y faces (fp32 needs the AA scheme)")
         return geom, params, "dense", desc, 1.0
     if name == "duct":
         geom = lb.build_duct_z(1024, 1024, 256)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
-        desc = "C5 slab: D3Q19 duct 1024x1024x256 along z, fp32"
+        desc = "C5 slab: D3Q19 duct 1024x1024x256 along z"
         return geom, params, "dense", desc, 1.0
     raise SystemExit(f"unknown workload {name}")
 
@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=100)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None)
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
+                    help="storage/arithmetic type (the reference's Simulation defaults to float64)")
     ap.add_argument("--tile", default="4,8,16",
                     help="tile edges x,y,z for tile layouts (4x8x16: measured best of 7 shapes, "
                          "profiles/sparse_r01.md; the API default is 8x8x8)")
@@ -272,6 +274,8 @@ def main():
     geom, params, layout, desc, rho0 = build_workload(workload)
     scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
     tile = tuple(int(v) for v in args.tile.split(","))
+    scalar = np.float32 if args.dtype == "f32" else np.float64
+    esz = np.dtype(scalar).itemsize
     if args.variants:
         for v in args.variants.split(","):
             # "3" selects LBM_STEP_VARIANT=3; "KEY=VAL;KEY=VAL" sets library switches
@@ -281,7 +285,7 @@ def main():
                     os.environ[k] = val
             else:
                 os.environ["LBM_STEP_VARIANT"] = v
-            sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
+            sim = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=local,
                                 scheme=scheme, tile=tile)
             sim.initialize(rho0)
             sim.step(args.warmup)
@@ -290,14 +294,14 @@ def main():
             nons = sim.active_node_count
             mlups = nons * args.steps / (ms / 1e3) / 1e6
             peak, _ = measured_peak()
-            alg = nons * PDF_BYTES_PER_NODE_F32 + int(sim.stats().meta_bytes_per_step)
+            alg = nons * 2 * 19 * esz + int(sim.stats().meta_bytes_per_step)
             frac = alg / (ms / args.steps / 1e3) / 1e9 / peak
             print(json.dumps({"workload": workload, "variant": v, "tile": args.tile, "mlups": round(mlups),
                               "frac": round(frac, 4), "alg_B_per_node": round(alg / nons, 2),
                               "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
         return
-    sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local, scheme=scheme,
+    sim = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=local, scheme=scheme,
                         tile=tile)
     sim.initialize(rho0)
     sim.step(args.warmup)
@@ -316,7 +320,7 @@ def main():
     # node, plus the flag / index bytes this design's step reads (dense: flag
     # words of non-uniform warp chunks + the uniform-chunk bitmap; tiles:
     # nbr27 + brick masks + flag words of live bricks)
-    alg_bytes = nons * PDF_BYTES_PER_NODE_F32 + int(st.meta_bytes_per_step)
+    alg_bytes = nons * 2 * 19 * esz + int(st.meta_bytes_per_step)
     achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
     sane = bool(np.isfinite(sim.total_mass()))
     sim.close()
@@ -331,7 +335,7 @@ def main():
         big = nx * ny * nz > (1 << 30)
         d2h = (1 if big else 4) * 8 * nx * ny * nz
         t0 = time.perf_counter()
-        s2 = lb.Simulation(geom, params, layout=layout, scalar=np.float32, device=local,
+        s2 = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=local,
                            scheme=scheme, tile=tile)
         t_setup = time.perf_counter() - t0
         s2.initialize(rho0)
@@ -367,7 +371,7 @@ def main():
     line = {
         "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": desc, "layout": layout, "scheme": scheme,
                    "tile": list(tile) if layout in ("tile", "pointer_tile") else None,
                    "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile")
@@ -385,8 +389,8 @@ def main():
                      "meta_bytes_per_launch": int(st.meta_bytes_per_step),
                      "copy_gbs": copy_gbs,
                      "frac_of_copy": (achieved / copy_gbs) if copy_gbs else None,
-                     "frac_152B": nons * 152 / (per_launch_ms / 1e3) / 1e9 / peak,
-                     "frac_156B": nons * 156 / (per_launch_ms / 1e3) / 1e9 / peak},
+                     "frac_152B": nons * 152 / (per_launch_ms / 1e3) / 1e9 / peak if esz == 4 else None,
+                     "frac_156B": nons * 156 / (per_launch_ms / 1e3) / 1e9 / peak if esz == 4 else None},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "finite": sane,
     }
