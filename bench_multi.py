@@ -59,7 +59,9 @@ def run_multi(args, rank, world, local):
         desc = (f"C2 weak scaling: D3Q19 channel 512x512x{512 * world} (z-periodic ring), "
                 "z-slab of 512^3 per GPU, fp32")
         periodic = True
-    sim = lb.Simulation(geom, params, layout="dense", scalar=np.float32, device=local, slab=spec)
+    scheme = args.scheme or "ab"
+    sim = lb.Simulation(geom, params, layout="dense", scalar=np.float32, device=local, slab=spec,
+                        scheme=scheme)
     connect_distributed(sim, periodic_z=periodic)
     sim.initialize(1.0)
     sim.step(args.warmup)
@@ -102,7 +104,8 @@ def run_multi(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": desc, "layout": "dense", "nodes_per_gpu": int(per_gpu_nodes),
+            "config": {"workload": desc, "layout": "dense", "scheme": scheme,
+                       "nodes_per_gpu": int(per_gpu_nodes),
                        "l2": "state per GPU >> 126 MB L2 (no flush needed)",
                        "parallelism": f"z-slab x{world}, fused peer-store halo (CUDA IPC)"},
             "mlups_per_gpu": mlups / world,
@@ -118,7 +121,8 @@ def run_multi(args, rank, world, local):
     # initialize + step(K) + macroscopic readback, wall clock, max over ranks
     dist.barrier()
     t0 = time.perf_counter()
-    s2 = lb.Simulation(geom, params, layout="dense", scalar=np.float32, device=local, slab=spec)
+    s2 = lb.Simulation(geom, params, layout="dense", scalar=np.float32, device=local, slab=spec,
+                       scheme=scheme)
     connect_distributed(s2, periodic_z=periodic)
     s2.initialize(1.0)
     s2.step(args.steps)

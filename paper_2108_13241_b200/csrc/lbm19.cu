@@ -227,6 +227,15 @@ dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g
 template <typename T>
 Halo<T> make_halo(const lbm_handle* h, int q) {
   Halo<T> H;
+  if (h->g.aa) {
+    // A-A: the neighbours' boundary planes themselves (lower slab's top plane,
+    // upper slab's plane 0) -- the neighbour step reads and writes them directly
+    for (int j = 0; j < 5; ++j) {
+      H.lo[j] = h->lo.on ? (T*)h->lo.f[0] + (size_t)kZm(j) * h->lo.ps + (size_t)h->lo.nz * h->g.plane : nullptr;
+      H.hi[j] = h->hi.on ? (T*)h->hi.f[0] + (size_t)kZp(j) * h->hi.ps + (size_t)h->g.plane : nullptr;
+    }
+    return H;
+  }
   for (int j = 0; j < 5; ++j) {
     H.lo[j] = h->lo.on ? (T*)h->lo.f[q] + (size_t)kZm(j) * h->lo.ps + (size_t)(h->lo.nz + 1) * h->g.plane
                        : nullptr;
@@ -390,9 +399,10 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
       for (int i = 0; i < Q; ++i) F.f[i] = (T*)post + (size_t)i * g.ps;
       dim3 grid((g.nxp + 127) / 128, g.ny, g.nz);
       if (h->parity == 0)
-        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om);
+        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om,
+                                                               make_halo<T>(h, 0));
       else
-        k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om);
+        k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, Halo<T>{});
     } else {
       if (h->n_tiles == 0) return 0;
       switch (g.tn) {
@@ -459,7 +469,10 @@ void preload_halo_kernels(const lbm_handle* h) {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_halo_wait);
   cudaFuncGetAttributes(&a, k_halo_signal);
-  if (!h->g.tiled) {
+  if (!h->g.tiled && h->g.aa) {
+    cudaFuncGetAttributes(&a, k_step_dense_aa<T, 1, D1>);
+    cudaFuncGetAttributes(&a, k_step_dense_aa<T, 0, D1>);
+  } else if (!h->g.tiled) {
     cudaFuncGetAttributes(&a, k_halo_push<T>);
     cudaFuncGetAttributes(&a, k_step_dense<T, 0, D1>);
     cudaFuncGetAttributes(&a, k_step_dense<T, 1, D1>);
@@ -706,7 +719,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
       if (d.periodic[a] && n3[a] % d.tile[a])
         return fail(LBM_EINVAL, "periodic axis %d needs extent %d divisible by the tile edge %d", a, n3[a], d.tile[a]);
   }
-  if (d.scheme == LBM_SCHEME_AA && nzg != d.nz) return fail(LBM_EINVAL, "the AA scheme is single-slab in this build");
+  if (d.scheme == LBM_SCHEME_AA && nzg != d.nz && is_tiled(d.layout))
+    return fail(LBM_EINVAL, "the AA scheme is single-slab for tile layouts in this build");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (d.device < 0 || d.device >= ndev) return fail(LBM_EINVAL, "device %d not present (%d devices)", d.device, ndev);
@@ -803,7 +817,7 @@ void lbm_destroy(lbm_t* h) {
   for (lbm_handle::Peer* pr : {&h->lo, &h->hi}) {
     if (pr->on && pr->ipc) {
       cudaIpcCloseMemHandle(pr->f[0]);
-      cudaIpcCloseMemHandle(pr->f[1]);
+      if (pr->f[1] != pr->f[0]) cudaIpcCloseMemHandle(pr->f[1]);
       cudaIpcCloseMemHandle(pr->sync);
     }
     pr->on = false;
@@ -1163,7 +1177,10 @@ int lbm_step_async(lbm_t* h, int64_t n) {
   const bool halo = halo_on(h);
   if (halo && h->halo_dirty && n > 0) {
     // ghost planes of `pre` after initialize / set_pdf: push, then signal
-    if (h->esize == 4) halo_push<float>(h); else halo_push<double>(h);
+    // (A-A reads the neighbours' planes directly: signal only)
+    if (!h->g.aa) {
+      if (h->esize == 4) halo_push<float>(h); else halo_push<double>(h);
+    }
     halo_signal(h);
     h->halo_dirty = false;
   }
@@ -1462,7 +1479,16 @@ static int pdf_io(lbm_t* h, int which, void* host, bool get) {
 }
 
 int lbm_get_pdf(lbm_t* h, int32_t which, void* out) { return pdf_io(h, which, out, true); }
+// A-A z-slab at an odd step count: pre_i of boundary nodes lives in the
+// neighbour's memory (the local ghost plane is a read-only mirror)
+static int aa_slab_write_guard(const lbm_t* h) {
+  if (h && h->g.aa && (h->lo.on || h->hi.on) && h->parity == 1)
+    return fail(LBM_ESTATE, "A-A z-slabs accept state writes at even step counts only");
+  return 0;
+}
+
 int lbm_set_pdf(lbm_t* h, int32_t which, const void* in) {
+  if (int rc = aa_slab_write_guard(h)) return rc;
   if (h) h->halo_dirty = true;
   return pdf_io(h, which, (void*)in, false);
 }
@@ -1516,6 +1542,7 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
 
 int lbm_get_field(lbm_t* h, int32_t which, void* out) { return field_io(h, which, out, true); }
 int lbm_set_field(lbm_t* h, int32_t which, const void* in) {
+  if (int rc = aa_slab_write_guard(h)) return rc;
   if (h) h->halo_dirty = true;
   return field_io(h, which, (void*)in, false);
 }
@@ -1591,7 +1618,7 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
 namespace {
 struct HaloBlob {
   uint32_t magic;
-  int32_t device, esize, nz, ny, nxp, tiled;
+  int32_t device, esize, nz, ny, nxp, tiled, aa;
   int64_t pid, ps;
   void* f[2];
   void* sync;
@@ -1603,7 +1630,8 @@ static_assert(sizeof(HaloBlob) <= LBM_HALO_BLOB_BYTES, "halo blob too large");
 
 int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
   if (b.magic != kHaloMagic) return fail(LBM_EINVAL, "not a halo blob");
-  if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp || b.tiled != h->g.tiled)
+  if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp || b.tiled != h->g.tiled ||
+      b.aa != h->g.aa)
     return fail(LBM_EINVAL, "neighbouring slab has a different dtype, layout family or x/y extent");
   if (b.pid == (int64_t)getpid()) {
     if (b.device != h->d.device) {
@@ -1621,7 +1649,10 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
     pr.ipc = false;
   } else {
     CK(cudaIpcOpenMemHandle(&pr.f[0], b.ipc_f[0], cudaIpcMemLazyEnablePeerAccess));
-    CK(cudaIpcOpenMemHandle(&pr.f[1], b.ipc_f[1], cudaIpcMemLazyEnablePeerAccess));
+    if (b.f[1] == b.f[0])  // A-A exporter: one buffer, mapped once
+      pr.f[1] = pr.f[0];
+    else
+      CK(cudaIpcOpenMemHandle(&pr.f[1], b.ipc_f[1], cudaIpcMemLazyEnablePeerAccess));
     void* sy = nullptr;
     CK(cudaIpcOpenMemHandle(&sy, b.ipc_sync, cudaIpcMemLazyEnablePeerAccess));
     pr.sync = (unsigned long long*)sy;
@@ -1637,7 +1668,7 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
 int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_export");
-  if (h->g.aa) return fail(LBM_EINVAL, "z-slab halos need the AB scheme in this build");
+  if (h->g.aa && h->g.tiled) return fail(LBM_EINVAL, "A-A z-slabs need a dense layout in this build");
   if (h->g.tiled && !h->gh[0]) return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
   DeviceGuard dg(h->d.device);
   HaloBlob b;
@@ -1651,13 +1682,14 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   b.pid = (int64_t)getpid();
   b.ps = h->g.ps;
   b.tiled = h->g.tiled;
+  b.aa = h->g.aa;
   // dense: the PDF buffers (ghost planes inside); tiles: the ghost-plane buffers
   void* const* ex = h->g.tiled ? h->gh : h->f;
   b.f[0] = ex[0];
-  b.f[1] = ex[1];
+  b.f[1] = ex[1] ? ex[1] : ex[0];  // A-A: one buffer
   b.sync = h->sync;
-  CK(cudaIpcGetMemHandle(&b.ipc_f[0], ex[0]));
-  CK(cudaIpcGetMemHandle(&b.ipc_f[1], ex[1]));
+  CK(cudaIpcGetMemHandle(&b.ipc_f[0], b.f[0]));
+  CK(cudaIpcGetMemHandle(&b.ipc_f[1], b.f[1]));
   CK(cudaIpcGetMemHandle(&b.ipc_sync, h->sync));
   memset(blob, 0, LBM_HALO_BLOB_BYTES);
   memcpy(blob, &b, sizeof(b));

@@ -340,11 +340,26 @@ __device__ __forceinline__ int opaque(int v) {
   return v;
 }
 
+// z-slabs under A-A: the neighbour step of a boundary plane reads and writes
+// the neighbouring slab's boundary plane directly (peer memory, H.hi = the
+// upper slab's plane 0, c_z = +1 directions; H.lo = the lower slab's top
+// plane, c_z = -1 directions).  By the single-owner property these locations
+// belong to this thread alone within the step; the per-step wait/signal
+// orders them against the neighbours' node-local steps.  The pushes are also
+// mirrored into this slab's own ghost plane, where the phase-1 readback
+// decoder (pre_index) finds them.
+template <typename T>
+__device__ __forceinline__ unsigned peer_row(const Geo& g, int x, int y) {
+  if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;  // present links wrap only on periodic axes
+  if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
+  return (unsigned)y * g.nxp + x;
+}
+
 template <typename T, int NB, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P, const uint32_t* __restrict__ flags,
                                                       const uint32_t* __restrict__ ubits,
                                                       const T* __restrict__ bcv, const T* __restrict__ bcr,
-                                                      Geo g, T om) {
+                                                      Geo g, T om, const Halo<T> H) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nxp) return;
@@ -369,6 +384,21 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
       for (int i = 1; i < Q; ++i)
         if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(P.f[i] + s);
     }
+    const bool top = z == g.nz - 1 && H.hi[0], bot = z == 0 && H.lo[0];
+    if (top || bot) {
+      // upstream across the cut: the neighbour slab's boundary plane
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (top) {
+          const int i = kZm(j);  // c_z = -1: pulls from z + 1, stored at F_U[opp(i) = kZp(j)]
+          if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = H.hi[j][peer_row<T>(g, x - cx(i), y - cy(i))];
+        }
+        if (bot) {
+          const int i = kZp(j);  // c_z = +1: pulls from z - 1, stored at F_L[opp(i) = kZm(j)]
+          if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = H.lo[j][peer_row<T>(g, x - cx(i), y - cy(i))];
+        }
+      }
+    }
     bc_collide<T>(f, w, bcv, bcr, om);
     // recompute the store addresses from opaque copies (measured: keeping the
     // 18 load addresses live at 64 registers is no faster)
@@ -379,6 +409,25 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
     for (int i = 1; i < Q; ++i) {
       T* dst = ((miss >> (i - 1)) & 1u) ? P.f[opp(i)] + s2 : P.f[i] + o2.up(s2, opp(i));
       *dst = f[i];
+    }
+    if (top || bot) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (top) {
+          const int i = kZp(j);  // pushed into the upper slab's plane 0 (the ghost copy stays as a mirror)
+          if ((miss >> (i - 1)) & 1u) continue;
+          H.hi[j][peer_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (bot) {
+          const int i = kZm(j);
+          if ((miss >> (i - 1)) & 1u) continue;
+          H.lo[j][peer_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+        }
+      }
+      __threadfence_system();
     }
   } else {
 #pragma unroll

@@ -9,20 +9,21 @@ import paper_2108_13241_b200 as lb
 from paper_2108_13241_b200.distributed import channel_slab, connect_local
 
 steps = 200
+scheme = sys.argv[1] if len(sys.argv) > 1 else "ab"
 params = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25)
 g, _ = channel_slab(512, 512, 512, 0, 1)
-one = lb.Simulation(g, params, scalar=np.float32)
+one = lb.Simulation(g, params, scalar=np.float32, scheme=scheme)
 one.initialize(1.0)
 one.step(20)
 one.step(steps)
 t1 = one.last_step_ms
 one.close()
-print({"slabs": 1, "ms_per_step": t1 / steps, "mlups": 512**3 * steps / t1 / 1e3}, flush=True)
+print({"scheme": scheme, "slabs": 1, "ms_per_step": t1 / steps, "mlups": 512**3 * steps / t1 / 1e3}, flush=True)
 for k in (2, 4):
     sims = []
     for r in range(k):
         gr, spec = channel_slab(512, 512, 512 // k, r, k)
-        sims.append(lb.Simulation(gr, params, scalar=np.float32, slab=spec))
+        sims.append(lb.Simulation(gr, params, scalar=np.float32, slab=spec, scheme=scheme))
     connect_local(sims, True)
     for s in sims:
         s.initialize(1.0)
@@ -37,7 +38,7 @@ for k in (2, 4):
         s.synchronize()
     wall = time.perf_counter() - t0
     ms = max(s.last_step_ms for s in sims)
-    print({"slabs": k, "ms_per_step": ms / steps, "wall_ms_per_step": wall * 1e3 / steps,
+    print({"scheme": scheme, "slabs": k, "ms_per_step": ms / steps, "wall_ms_per_step": wall * 1e3 / steps,
            "mlups": 512**3 * steps / ms / 1e3}, flush=True)
     for s in sims:
         s.close()

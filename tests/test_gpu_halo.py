@@ -90,6 +90,40 @@ def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
     assert np.array_equal(single.canonical_state(), ref.pre)
 
 
+@pytest.mark.parametrize("nslab,periodic_z,dtype", [(2, False, np.float32), (3, True, np.float64),
+                                                    (4, False, np.float32), (2, True, np.float32)])
+def test_aa_slabs_in_process_bitwise(nslab, periodic_z, dtype):
+    """A-A z-slabs: the neighbour step reads and writes the neighbouring
+    slab's boundary plane directly; odd and even step counts decode to the
+    single-domain AB run bitwise."""
+    c = random_mixed_geometry3(14, n=(19, 12, 17), periodic_z=periodic_z)
+    geom = to_geometry(c)
+    params = _params(1.3)
+    single = lb.Simulation(geom, params, scalar=dtype)
+    single.initialize(1.0)
+    sims = []
+    for z0, z1 in split_z(17, nslab):
+        g, spec = slab_geometry(geom, z0, z1)
+        sims.append(lb.Simulation(g, params, scalar=dtype, slab=spec, scheme="aa"))
+    connect_local(sims, periodic_z)
+    for s in sims:
+        s.initialize(1.0)
+    for chunk in (1, 2, 1, 37):
+        single.step(chunk)
+        for s in sims:
+            s.step(chunk, block=False)
+        for s in sims:
+            s.synchronize()
+        got = np.concatenate([s.canonical_state() for s in sims], axis=1)
+        assert np.array_equal(got, single.canonical_state()), (chunk, single.step_count)
+        rho = np.concatenate([s.macroscopic_fields()[0] for s in sims], axis=0)
+        assert np.array_equal(rho, single.macroscopic_fields()[0])
+    # odd step count: state writes are refused (boundary pre_i lives in the neighbour)
+    assert sims[0].step_count % 2 == 1
+    with pytest.raises(RuntimeError):
+        sims[0].set_state(sims[0].canonical_state())
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -106,8 +140,9 @@ def _ipc_worker(rank, world, port, out_dir, layout="dense"):
     geom = to_geometry(c)
     z0, z1 = split_z(14, world)[rank]
     g, spec = slab_geometry(geom, z0, z1)
-    sim = lb.Simulation(g, _params(1.1), layout=layout, scalar=np.float32, slab=spec, device=0,
-                        tile=(8, 4, 1))
+    scheme = "aa" if layout.endswith("-aa") else "ab"
+    sim = lb.Simulation(g, _params(1.1), layout=layout.replace("-aa", ""), scalar=np.float32, slab=spec,
+                        device=0, tile=(8, 4, 1), scheme=scheme)
     connect_distributed(sim, periodic_z=True)
     sim.initialize(1.0)
     sim.step(25)
@@ -117,7 +152,7 @@ def _ipc_worker(rank, world, port, out_dir, layout="dense"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["dense", "pointer_tile"])
+@pytest.mark.parametrize("layout", ["dense", "pointer_tile", "dense-aa"])
 def test_slabs_two_processes_ipc_bitwise(tmp_path, layout):
     import torch.multiprocessing as mp
     mp.spawn(_ipc_worker, args=(2, _free_port(), str(tmp_path), layout), nprocs=2, join=True)
