@@ -76,7 +76,13 @@ template <> struct ar<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
-  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  // 0 / b for finite-or-infinite nonzero b is a signed zero (sign(a) ^ sign(b));
+  // __fdiv_rn sends a zero dividend down its slow path (FCHK), which every
+  // node of a flow with an exactly zero momentum component would pay
+  static __device__ __forceinline__ float div(float a, float b) {
+    if (a == 0.f && b != 0.f && b == b) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & 0x80000000);
+    return __fdiv_rn(a, b);
+  }
 #else
   static inline float add(float a, float b) { return a + b; }
   static inline float sub(float a, float b) { return a - b; }
@@ -89,7 +95,11 @@ template <> struct ar<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) {
+    if (a == 0.0 && b != 0.0 && b == b)
+      return __longlong_as_double((__double_as_longlong(a) ^ __double_as_longlong(b)) & (long long)0x8000000000000000ULL);
+    return __ddiv_rn(a, b);
+  }
 #else
   static inline double add(double a, double b) { return a + b; }
   static inline double sub(double a, double b) { return a - b; }
