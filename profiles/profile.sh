@@ -11,9 +11,12 @@ for W in $WLS; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
       --log-file gpurun_out/launches_${TAG}_${W}.csv \
       python bench.py --workload $W --steps 5 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 \
+  # one step-kernel launch after 600 steps: the flow has reached the whole
+  # domain (early steps are mostly fluid at rest, whose zero momenta take
+  # cheaper arithmetic paths)
+  LBM_GRAPH=0 ncu --set full --clock-control none --import-source on -k regex:k_step -s 600 -c 1 \
       -o gpurun_out/prof_${TAG}_${W} -f \
-      python bench.py --workload $W --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_${TAG}_${W}.log 2>&1
+      python bench.py --workload $W --steps 2 --warmup 600 --no-cpu --no-e2e > gpurun_out/ncu_${TAG}_${W}.log 2>&1
   # export the raw page and the source-line hot spots; keep the .ncu-rep only
   # for the first workload (gpurun copies back at most 64 MiB)
   ncu -i gpurun_out/prof_${TAG}_${W}.ncu-rep --page raw --csv > gpurun_out/raw_${TAG}_${W}.csv 2>/dev/null
