@@ -314,7 +314,9 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
-  if (var == 0 && h->auto_wlist && !h->variant_set) var = 5;
+  // default kernel choice (measured, profiles/sparse_r01.md): warp work list
+  // for sparse tiles, else the barrier-free CTA-per-tile kernel
+  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 5 : 7;
   if (TH.on) {  // z-slab: the live-brick kernel with the ghost-plane exchange
     k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
         pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
@@ -331,6 +333,10 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
       cudaFuncSetAttribute(k_step_tiles_s<T, TN, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
       k_step_tiles_s<T, TN, MB><<<nt, BT, SMEM, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
                                                              h->bmask);
+      return;
+    }
+    if (var == 7) {
+      k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
       return;
     }
     if (var == 5) {

@@ -250,6 +250,61 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
   }
 }
 
+// MODE 7: the live-brick CTA-per-tile kernel without the shared-memory
+// neighbour table and its block barrier: every warp keeps the 27 relative
+// tile offsets in lanes 0-26 and fetches them with shuffles (all lanes take
+// part, so the offsets are formed before dead lanes leave the iteration).
+template <typename T, int TN, int MINB>
+__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
+k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
+               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+               const uint32_t* __restrict__ bmask) {
+  constexpr int BT = TN < 256 ? TN : 256;
+  const int t = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  int srel = 0;
+  if (lane < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + lane);
+    srel = v < 0 ? 0 : (v - t) * (Q * TN);
+  }
+  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
+  T* __restrict__ tp = post + (size_t)t * (Q * TN);
+  const TileBricks tw(bmask, t, g, TN, true);
+#pragma unroll 1
+  for (int k = threadIdx.x - lane; k < tw.work; k += BT) {  // whole warps
+    const int kk = k + lane;
+    bool in;
+    const int l = tw.slot(kk, in);
+    const uint32_t w = tw.flag(flags, t, TN, l, in);
+    const bool live = flag_type(w) != SOLID;
+    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+    const TileUp up(g, l);
+    int off[Q];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
+    if (!live) {
+      if (zfill && in) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+      }
+      continue;
+    }
+    const uint32_t miss = ~w & kMaskBits;
+    T f[Q];
+    f[0] = __ldg(tb + l);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + off[i]);
+    if (miss) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+  }
+}
+
 // Shared-memory tile staging (MODE 6): pass 1 stages the tile's live bricks
 // (each thread its own nodes' 19 values, coalesced) in shared memory; after
 // one barrier, pass 2 gathers in-tile upstream values from shared memory and
