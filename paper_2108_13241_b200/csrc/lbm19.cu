@@ -23,6 +23,8 @@
 //          block contiguous (8^3 fp32 -> 2 KB).
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -40,6 +42,12 @@
 #include "lbm19.h"
 
 using namespace lbm;
+
+// NVTX ranges (header-only NVTX3; no-ops unless a tool such as nsys/ncu attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------ error plumbing
 static thread_local std::string g_err;
@@ -865,6 +873,7 @@ struct PhaseTimer {
 int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const int32_t* bc_index,
                      const uint8_t* ghost_lo, const uint8_t* ghost_hi, const uint8_t* bc_kind,
                      const double* bc_vel, const double* bc_rho, int32_t nb) {
+  NvtxRange nv("lbm_set_geometry");
   if (!h || !type || !orient || !bc_index) return fail(LBM_EINVAL, "NULL geometry array");
   if (nb < 0 || nb > 255) return fail(LBM_EINVAL, "boundary table holds %d entries; at most 255 supported", nb);
   if (nb > 0 && (!bc_kind || !bc_vel || !bc_rho)) return fail(LBM_EINVAL, "NULL boundary table");
@@ -1177,6 +1186,7 @@ int lbm_set_omega(lbm_t* h, double omega) {
 
 int lbm_step_async(lbm_t* h, int64_t n) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
+  NvtxRange nv("lbm_step");
   if (n < 0) return fail(LBM_EINVAL, "n_steps must be >= 0, got %lld", (long long)n);
   if (!h->initialized) return fail(LBM_ESTATE, "initialize() must run before stepping");
   DeviceGuard dg(h->d.device);
@@ -1243,6 +1253,7 @@ int lbm_step_async(lbm_t* h, int64_t n) {
 
 int lbm_synchronize(lbm_t* h) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
+  NvtxRange nv("lbm_synchronize");
   DeviceGuard dg(h->d.device);
   if (!h->pending) return 0;
   h->pending = false;
@@ -1279,6 +1290,7 @@ int chunk_planes(const lbm_handle* h, long long bytes_per_node) {
 
 int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* uz) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
+  NvtxRange nv("lbm_get_macroscopic");
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   DeviceGuard dg(h->d.device);
   const Geo g = rb_geo(h);
