@@ -100,6 +100,7 @@ struct lbm_handle {
   int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
   void* gh[2] = {nullptr, nullptr};  // tile slabs: ghost planes per buffer, [lo | hi] x 5 x ny x nx
   int* items = nullptr;   // warp work list (tile << 4 | live-brick group), MODE 5
+  unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
   int n_items = 0;
   bool auto_wlist = false;  // default tile kernel = warp work list (sparse tiles)
   bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
@@ -204,6 +205,8 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->order);
   dev_free(h->items);
   h->items = nullptr;
+  dev_free(h->lut);
+  h->lut = nullptr;
   h->n_items = 0;
   dev_free(h->gh[0]);
   dev_free(h->gh[1]);
@@ -344,14 +347,15 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
       return;
     }
     if (var == 7) {
-      k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask);
+      k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask,
+                                                         h->lut);
       return;
     }
     if (var == 5) {
       constexpr int MW = sizeof(T) == 4 ? 6 : 3;
       if (h->n_items)
         k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
-            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items);
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items, h->lut);
       return;
     }
     if (var == 3 || var == 4 || var == 1 || var == 2) {
@@ -1067,6 +1071,29 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
                         (h->auto_wlist ? (long long)h->n_items * 4 : 0);
       }
       h->sm.rank = h->rank;
+      {
+        // per-slot neighbour table for the tile kernels (TileUpLUT)
+        std::vector<unsigned long long> lt(g.tn);
+        for (int l = 0; l < g.tn; ++l) {
+          int lx, ly, lz;
+          brick_inv(g, l, lx, ly, lz);
+          const int e[3] = {g.ex, g.ey, g.ez}, c[3] = {lx, ly, lz};
+          unsigned long long w = 0;
+          for (int a = 0; a < 3; ++a) {
+            auto br = [&](int v) { return a == 0 ? brick_x(g, v) : (a == 1 ? brick_y(g, v) : brick_z(g, v)); };
+            const int own = br(c[a]);
+            const bool cm = c[a] == 0, cp = c[a] == e[a] - 1;
+            const int mm = br(cm ? e[a] - 1 : c[a] - 1) - own, mp = br(cp ? 0 : c[a] + 1) - own;
+            w |= (unsigned long long)(mm < 0 ? -mm : mm) << (18 * a);
+            w |= (unsigned long long)(mp < 0 ? -mp : mp) << (18 * a + 9);
+            w |= (unsigned long long)cm << (54 + 2 * a);
+            w |= (unsigned long long)cp << (55 + 2 * a);
+          }
+          lt[l] = w;
+        }
+        if ((rc = dev_alloc(h, &h->lut, lt.size() * 8))) goto done;
+        CK(cudaMemcpy(h->lut, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice));
+      }
       // z-slab ghost planes (tile layouts keep them outside the tile storage)
       h->has_glo = ghost_lo != nullptr;
       h->has_ghi = ghost_hi != nullptr;

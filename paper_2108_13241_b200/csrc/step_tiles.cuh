@@ -89,6 +89,39 @@ struct TileUp {
   __device__ __forceinline__ int at(const int* srel, int i) const { return srel[code(i)] + loc(i); }
 };
 
+// The same offsets from a per-slot table (one u64 per in-tile slot, built
+// on the host for the handle's tile shape, L1-resident): bits 0-53 hold the
+// six in-tile brick-order deltas' magnitudes (9 bits each: x-, x+, y-, y+,
+// z-, z+), bits 54-59 whether the neighbour lies across the tile face (the
+// delta is then positive -- a wrap inside the neighbour tile -- else
+// negative for "-" and positive for "+").
+struct TileUpLUT {
+  int l, dxm, dxp, dym, dyp, dzm, dzp, cxm, cxp, cym, cyp, czm, czp;
+  __device__ __forceinline__ TileUpLUT(const unsigned long long* __restrict__ lut, int slot) : l(slot) {
+    const unsigned long long e = __ldg(lut + slot);
+    const int mag[6] = {(int)(e & 511), (int)(e >> 9 & 511), (int)(e >> 18 & 511), (int)(e >> 27 & 511),
+                        (int)(e >> 36 & 511), (int)(e >> 45 & 511)};
+    const unsigned cr = (unsigned)(e >> 54) & 63u;
+    dxm = (cr & 1) ? mag[0] : -mag[0];
+    dxp = mag[1] * ((cr & 2) ? -1 : 1);
+    dym = (cr & 4) ? mag[2] : -mag[2];
+    dyp = mag[3] * ((cr & 8) ? -1 : 1);
+    dzm = (cr & 16) ? mag[4] : -mag[4];
+    dzp = mag[5] * ((cr & 32) ? -1 : 1);
+    cxm = (cr & 1) ? -1 : 0, cxp = (cr & 2) ? 1 : 0;
+    cym = (cr & 4) ? -3 : 0, cyp = (cr & 8) ? 3 : 0;
+    czm = (cr & 16) ? -9 : 0, czp = (cr & 32) ? 9 : 0;
+  }
+  __device__ __forceinline__ int code(int i) const {
+    return 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) + (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
+           (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
+  }
+  __device__ __forceinline__ int loc(int i) const {
+    return l + (cx(i) == 1 ? dxm : (cx(i) == -1 ? dxp : 0)) + (cy(i) == 1 ? dym : (cy(i) == -1 ? dyp : 0)) +
+           (cz(i) == 1 ? dzm : (cz(i) == -1 ? dzp : 0));
+  }
+};
+
 // stage the 27 neighbour ranks as relative element offsets (absent: 0, i.e.
 // the own tile -- such links are masked)
 template <int TN>
@@ -258,7 +291,7 @@ template <typename T, int TN, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask) {
+               const uint32_t* __restrict__ bmask, const unsigned long long* __restrict__ lut) {
   constexpr int BT = TN < 256 ? TN : 256;
   const int t = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -278,7 +311,7 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
     const uint32_t w = tw.flag(flags, t, TN, l, in);
     const bool live = flag_type(w) != SOLID;
     const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    const TileUp up(g, l);
+    const TileUpLUT up(lut, l);
     int off[Q];
 #pragma unroll
     for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
@@ -393,7 +426,8 @@ template <typename T, int TN, int MINB>
 __global__ void __launch_bounds__(256, MINB)
 k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask, const int* __restrict__ items, int n_items) {
+               const uint32_t* __restrict__ bmask, const int* __restrict__ items, int n_items,
+               const unsigned long long* __restrict__ lut) {
   const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
@@ -433,7 +467,7 @@ k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
   // every lane must take part in the shuffles: dead lanes compute garbage
   // addresses they never use
-  const TileUp up(g, l);
+  const TileUpLUT up(lut, l);
   int off[Q];
 #pragma unroll
   for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
