@@ -380,7 +380,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": desc, "layout": layout, "scheme": scheme,
                    "tile": list(tile) if layout in ("tile", "pointer_tile") else None,
-                   "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile (shuffled nbr27)")
+                   "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile")
                                    if layout in ("tile", "pointer_tile") else None),
                    "nodes": int(st.n_nodes),
                    "non_solid_nodes": int(nons), "tiles": int(st.n_tiles),

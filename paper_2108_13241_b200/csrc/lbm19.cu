@@ -103,6 +103,7 @@ struct lbm_handle {
   unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
   int n_items = 0;
   bool auto_wlist = false;  // default tile kernel = warp work list (sparse tiles)
+  double live_frac = 1.0;   // live bricks / brick slots of the kept tiles
   bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
   int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows, 3 z-groups of `pencil` layers
   int pencil = 4;
@@ -325,9 +326,10 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
-  // default kernel choice (measured, profiles/sparse_r01.md): warp work list
-  // for sparse tiles, else the barrier-free CTA-per-tile kernel
-  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 5 : 7;
+  // default kernel choice by live-brick fraction (measured, profiles/sparse_r01.md):
+  // < 0.70 warp work list + exact per-link select (8); < 0.85 CTA per tile +
+  // select (10); fuller tiles the speculative CTA-per-tile kernel (7)
+  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : (h->live_frac < 0.85 ? 10 : 7);
   if (TH.on) {  // z-slab: the live-brick kernel with the ghost-plane exchange
     k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
         pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
@@ -351,10 +353,18 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
                                                          h->lut);
       return;
     }
-    if (var == 5) {
+    if (var == 10) {
+      k_step_tiles_x<T, TN, M, true><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                               h->bmask, h->lut);
+      return;
+    }
+    if (var == 5 || var == 8) {
       constexpr int MW = sizeof(T) == 4 ? 6 : 3;
-      if (h->n_items)
+      if (h->n_items && var == 5)
         k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items, h->lut);
+      else if (h->n_items)
+        k_step_tiles_w<T, TN, MW, true><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
             pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items, h->lut);
       return;
     }
@@ -1065,6 +1075,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         // there, -2 % on fuller tiles (profiles/sparse_r01.md)
         const double live_frac = T > 0 ? (double)live / ((double)T * (g.tn / bn)) : 1.0;
         h->auto_wlist = h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.7;
+        h->live_frac = live_frac;
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag
         // words; the work list when it is used
         h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4 +
@@ -1655,7 +1666,8 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
   s->scheme = h->d.scheme;
-  s->tile_work_list = (h->auto_wlist && !h->variant_set) || (h->g.tiled && h->variant == 5) ? 1 : 0;
+  s->tile_work_list =
+      (h->auto_wlist && !h->variant_set) || (h->g.tiled && (h->variant == 5 || h->variant == 8)) ? 1 : 0;
   return 0;
 }
 

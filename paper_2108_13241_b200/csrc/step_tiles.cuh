@@ -287,7 +287,7 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
 // neighbour table and its block barrier: every warp keeps the 27 relative
 // tile offsets in lanes 0-26 and fetches them with shuffles (all lanes take
 // part, so the offsets are formed before dead lanes leave the iteration).
-template <typename T, int TN, int MINB>
+template <typename T, int TN, int MINB, bool SEL = false>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
@@ -326,8 +326,9 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
     T f[Q];
     f[0] = __ldg(tb + l);
 #pragma unroll
-    for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + off[i]);
-    if (miss) {
+    for (int i = 1; i < Q; ++i)  // SEL: masked links never fetch the (solid) upstream slot
+      f[i] = __ldg(tb + ((SEL && ((miss >> (opp(i) - 1)) & 1u)) ? opp(i) * TN + l : i * TN + off[i]));
+    if (!SEL && miss) {
 #pragma unroll
       for (int i = 1; i < Q; ++i)
         if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
@@ -422,7 +423,7 @@ k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
 // lane idles for a tile's dead bricks or its last partial pass and no CTA
 // slot is held by a nearly empty tile.  The 27 neighbour offsets live in
 // lanes 0-26 and are fetched with shuffles.
-template <typename T, int TN, int MINB>
+template <typename T, int TN, int MINB, bool SEL = false>
 __global__ void __launch_bounds__(256, MINB)
 k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
@@ -482,8 +483,9 @@ k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   T f[Q];
   f[0] = __ldg(tb + l);
 #pragma unroll
-  for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + off[i]);
-  if (miss) {
+  for (int i = 1; i < Q; ++i)  // SEL: masked links never fetch the (solid) upstream slot
+    f[i] = __ldg(tb + ((SEL && ((miss >> (opp(i) - 1)) & 1u)) ? opp(i) * TN + l : i * TN + off[i]));
+  if (!SEL && miss) {
 #pragma unroll
     for (int i = 1; i < Q; ++i)
       if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);

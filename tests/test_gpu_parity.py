@@ -350,7 +350,7 @@ def test_launch_configuration_does_not_change_results(monkeypatch):
     ref = run("dense", LBM_GRAPH="0")
     for v in ("0", "1", "2", "3", "8"):
         assert np.array_equal(run("dense", LBM_STEP_VARIANT=v), ref), v
-    for v in ("0", "1", "2", "3", "4", "5", "6", "7"):
+    for v in ("0", "1", "2", "3", "4", "5", "6", "7", "8", "10"):
         assert np.array_equal(run("pointer_tile", LBM_STEP_VARIANT=v), ref), v
     for order in ("morton", "pencil:2", "z:2"):
         assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order), ref), order
