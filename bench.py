@@ -277,6 +277,14 @@ def main():
 
     import paper_2108_13241_b200 as lb
     workload = args.workload or "channel512"
+    # CPU baseline first, before this process creates a CUDA context (measured
+    # ~40 % slower afterwards on the shared host: profiles/cpu_baseline_check_r01.txt)
+    cpu = None
+    if not args.no_cpu and not args.variants:
+        try:
+            cpu = cpu_baseline(workload)
+        except Exception as exc:  # reported, never fatal for the GPU number
+            cpu = {"value": None, "error": repr(exc)}
     geom, params, layout, desc, rho0 = build_workload(workload)
     scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
     tile = tuple(int(v) for v in args.tile.split(","))
@@ -367,12 +375,6 @@ def main():
     except Exception:
         copy_gbs = None
 
-    cpu = None
-    if not args.no_cpu:
-        try:
-            cpu = cpu_baseline(workload)
-        except Exception as exc:  # reported, never fatal for the GPU number
-            cpu = {"value": None, "error": repr(exc)}
 
     line = {
         "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
