@@ -396,11 +396,13 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
-  constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap
+  constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap (48)
   if (h->parity == 0)
-    k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order,
+                                                            h->lut);
   else
-    k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order);
+    k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order,
+                                                           h->lut);
 }
 
 // one step from `pre` into `post` (AB); AA updates `post` (== pre) in place

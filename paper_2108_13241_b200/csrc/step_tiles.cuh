@@ -502,45 +502,58 @@ template <typename T, int TN, int NB, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                 const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-                const uint32_t* __restrict__ bmask, const int* __restrict__ order) {
+                const uint32_t* __restrict__ bmask, const int* __restrict__ order,
+                const unsigned long long* __restrict__ lut) {
   constexpr int BT = TN < 256 ? TN : 256;
-  __shared__ int srel[27];
   const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
-  if (NB) stage_nbr<TN>(srel, nbr27, t);
+  const int lane = threadIdx.x & 31;
+  // neighbour ranks in lanes 0-26 (shuffles; no shared table, no barrier)
+  int srel = 0;
+  if (NB && lane < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + lane);
+    srel = v < 0 ? 0 : (v - t) * (Q * TN);
+  }
   T* __restrict__ tb = F + (size_t)t * (Q * TN);
   const TileBricks tw(bmask, t, g, TN, true);
-  if (NB) __syncthreads();
 #pragma unroll 1
-  for (int k = threadIdx.x; k < tw.work; k += BT) {
+  for (int k = threadIdx.x - lane; k < tw.work; k += BT) {  // whole warps
     bool in;
-    const int l = tw.slot(k, in);
+    const int l = tw.slot(k + lane, in);
     const uint32_t w = tw.flag(flags, t, TN, l, in);
-    if (flag_type(w) == SOLID) continue;  // no zero-fill under AA (see k_step_dense_aa)
-    const uint32_t miss = ~w & kMaskBits;
-    T f[Q];
-    f[0] = LDA(tb + l);
-    if (NB) {
-      const TileUp up(g, l);
+    const bool live = flag_type(w) != SOLID;  // no zero-fill under AA (see k_step_dense_aa)
+    if (!NB) {
+      if (!live) continue;
+      T f[Q];
 #pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + opp(i) * TN + up.at(srel, i));
-      if (miss) {
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-          if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(tb + i * TN + l);
-      }
-      bc_collide<T>(f, w, bcv, bcr, om);
-      const int l2 = opaque(l);
-      const TileUp up2(g, l2);
-      tb[l2] = f[0];
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + up2.at(srel, opp(i))] = f[i];
-    } else {
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
+      for (int i = 0; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
       bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
       for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
+      continue;
+    }
+    // neighbour step: the whole warp stays converged (solid lanes compute on
+    // zeros and store nothing) so the offsets can be re-formed by shuffles
+    // after the collision instead of being held in 18 registers
+    const uint32_t miss = ~w & kMaskBits;
+    T f[Q];
+    {
+      const TileUpLUT up(lut, l);
+      f[0] = live ? LDA(tb + l) : (T)0;
+#pragma unroll
+      for (int i = 1; i < Q; ++i) {
+        const int off = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
+        // exact per-link select: a masked link reads the node's own F[i]
+        f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? i * TN + l : opp(i) * TN + off)) : (T)0;
+      }
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+    const int l2 = opaque(l);
+    const TileUpLUT up2(lut, l2);
+    if (live) tb[l2] = f[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
+      if (live) tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + off] = f[i];
     }
   }
 }
