@@ -330,9 +330,14 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   // < 0.70 warp work list + exact per-link select (8); < 0.85 CTA per tile +
   // select (10); fuller tiles the speculative CTA-per-tile kernel (7)
   if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : (h->live_frac < 0.85 ? 10 : 7);
-  if (TH.on) {  // z-slab: the live-brick kernel with the ghost-plane exchange
-    k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
-        pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
+  if (TH.on) {  // z-slab: a live-brick kernel with the ghost-plane exchange
+    if constexpr (TN == 512) {
+      k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true><<<nt, BT, 0, h->stream>>>(
+          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->lut, TH);
+    } else {
+      k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
+          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
+    }
     return;
   }
   // measured alternatives (LBM_STEP_VARIANT, profiles/sparse_r01.md), built
@@ -490,7 +495,10 @@ template <typename T, int TN>
 void preload_tiles(cudaFuncAttributes* a) {
   constexpr int BT = TN < 256 ? TN : 256;
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
-  cudaFuncGetAttributes(a, k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true>);
+  if constexpr (TN == 512)
+    cudaFuncGetAttributes(a, k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true>);
+  else
+    cudaFuncGetAttributes(a, k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true>);
 }
 
 template <typename T>

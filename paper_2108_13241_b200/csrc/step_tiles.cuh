@@ -287,13 +287,24 @@ k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __
 // neighbour table and its block barrier: every warp keeps the 27 relative
 // tile offsets in lanes 0-26 and fetches them with shuffles (all lanes take
 // part, so the offsets are formed before dead lanes leave the iteration).
-template <typename T, int TN, int MINB, bool SEL = false>
+template <typename T, int TN, int MINB, bool SEL = false, bool CUT = false>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask, const unsigned long long* __restrict__ lut) {
+               const uint32_t* __restrict__ bmask, const unsigned long long* __restrict__ lut,
+               const TileHalo<T> TH = TileHalo<T>{}) {
   constexpr int BT = TN < 256 ? TN : 256;
   const int t = blockIdx.x;
+  // z-slab cut (CUT): tiles on the first / last tile plane exchange their
+  // boundary nodes' c_z populations through ghost planes (uniform per CTA)
+  int tz0 = 0, tx0 = 0, ty0 = 0;
+  bool cut = false;
+  if (CUT) {
+    tx0 = __ldg(TH.tiles + 3 * t) * g.ex;
+    ty0 = __ldg(TH.tiles + 3 * t + 1) * g.ey;
+    tz0 = __ldg(TH.tiles + 3 * t + 2) * g.ez;
+    cut = tz0 == 0 || tz0 + g.ez >= g.nz;
+  }
   const int lane = threadIdx.x & 31;
   int srel = 0;
   if (lane < 27) {
@@ -333,9 +344,18 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
       for (int i = 1; i < Q; ++i)
         if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
     }
+    int x = 0, y = 0, z = -1;
+    if (CUT && cut) {
+      brick_inv(g, l, x, y, z);
+      x += tx0;
+      y += ty0;
+      z += tz0;
+      tile_ghost_gather<T>(f, miss, TH, g, x, y, z);
+    }
     bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
     for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+    if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
   }
 }
 

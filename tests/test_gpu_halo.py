@@ -58,7 +58,9 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     ("pointer_tile", (8, 4, 4), 3, True, np.float64),
     ("pointer_tile", (4, 4, 2), 5, True, np.float32),
     ("tile", (8, 8, 4), 2, True, np.float32),
-    ("pointer_tile", (8, 8, 8), 2, False, np.float64)])
+    ("pointer_tile", (8, 8, 8), 2, False, np.float64),
+    ("pointer_tile", (4, 8, 16), 2, False, np.float32),
+    ("pointer_tile", (8, 8, 8), 3, True, np.float32)])
 def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
     """Sparse z-slabs: cuts on tile planes balanced by non-solid count; the
     boundary tiles exchange through ghost planes inside the step kernel."""
