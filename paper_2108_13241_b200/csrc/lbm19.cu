@@ -99,7 +99,7 @@ struct lbm_handle {
   int* nbr27 = nullptr;   // (T, 27)
   int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
   void* gh[2] = {nullptr, nullptr};  // tile slabs: ghost planes per buffer, [lo | hi] x 5 x ny x nx
-  int* items = nullptr;   // warp work list (tile << 4 | live-brick group), MODE 5
+  uint32_t* items = nullptr;  // warp work list, 4 words per warp (tile, brick bytes x2, uniform | count), MODE 5/8
   unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
   int n_items = 0;
   bool auto_wlist = false;  // default tile kernel = warp work list (sparse tiles)
@@ -327,9 +327,9 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
   // default kernel choice by live-brick fraction (measured, profiles/sparse_r01.md):
-  // < 0.70 warp work list + exact per-link select (8); < 0.85 CTA per tile +
-  // select (10); fuller tiles the speculative CTA-per-tile kernel (7)
-  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : (h->live_frac < 0.85 ? 10 : 7);
+  // < 0.85 warp work list + exact per-link select (8); fuller tiles the
+  // speculative CTA-per-tile kernel (7)
+  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : 7;
   if (TH.on) {  // z-slab: a live-brick kernel with the ghost-plane exchange
     if constexpr (TN == 512) {
       k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true><<<nt, BT, 0, h->stream>>>(
@@ -367,10 +367,10 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
       constexpr int MW = sizeof(T) == 4 ? 6 : 3;
       if (h->n_items && var == 5)
         k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
-            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items, h->lut);
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
       else if (h->n_items)
         k_step_tiles_w<T, TN, MW, true><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
-            pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->items, h->n_items, h->lut);
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
       return;
     }
     if (var == 3 || var == 4 || var == 1 || var == 2) {
@@ -402,6 +402,22 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
   constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap (48)
+  if constexpr (TN == 512) {
+    // the warp work list where the AB step would use it (or when variant 5/8 is forced)
+    const bool wl = h->variant_set ? (h->variant == 5 || h->variant == 8) : h->auto_wlist;
+    if (wl) {
+      if (!h->n_items) return;
+      const unsigned nb = (unsigned)((h->n_items + 7) / 8);
+      const uint4* it = (const uint4*)h->items;
+      if (h->parity == 0)
+        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 3><<<nb, 256, 0, h->stream>>>(
+            F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
+      else
+        k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 256, 0, h->stream>>>(
+            F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
+      return;
+    }
+  }
   if (h->parity == 0)
     k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order,
                                                             h->lut);
@@ -1065,31 +1081,48 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         CK(cudaStreamSynchronize(h->stream));
         long long live = 0, uni = 0;
         for (size_t k = 0; k < hb.size(); ++k) (k % 8 < 4 ? live : uni) += __builtin_popcount(hb[k]);
-        // warp work list: groups of (32 / bricksize) live bricks per tile
+        // warp work list: groups of (32 / bricksize) live bricks per tile, each
+        // item decoded on the host into {tile, brick byte per lane group (two
+        // words), uniform bits | count << 8}, so a warp reaches its data loads
+        // after one dependent load instead of walking the brick masks
         {
-          const int per = 32 / bn;
-          std::vector<int> it;
-          it.reserve((size_t)(live / per + T));
+          const int per = 32 / bn;  // 4 (fp32 2x2x2 bricks) or 8 (fp64 2x2x1)
+          std::vector<uint32_t> it;
+          it.reserve((size_t)(live / per + T) * 4);
           for (long long t = 0; t < T; ++t) {
-            int nl = 0;
-            for (int q = 0; q < 4; ++q) nl += __builtin_popcount(hb[8 * t + q]);
-            for (int gi = 0; gi * per < nl; ++gi) it.push_back((int)(t << 4 | gi));
+            uint32_t rec[4] = {(uint32_t)t, 0u, 0u, 0u};
+            int k = 0;
+            for (int b = 0; b < 128; ++b) {
+              if (!((hb[8 * t + (b >> 5)] >> (b & 31)) & 1u)) continue;
+              rec[1 + k / 4] |= (uint32_t)b << (8 * (k & 3));
+              if ((hb[8 * t + 4 + (b >> 5)] >> (b & 31)) & 1u) rec[3] |= 1u << k;
+              if (++k == per) {
+                rec[3] |= (uint32_t)k << 8;
+                it.insert(it.end(), rec, rec + 4);
+                rec[1] = rec[2] = rec[3] = 0u;
+                k = 0;
+              }
+            }
+            if (k) {
+              rec[3] |= (uint32_t)k << 8;
+              it.insert(it.end(), rec, rec + 4);
+            }
           }
           pt.mark("brick masks to host + work list");
-          h->n_items = (int)it.size();
-          if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 1) * 4))) goto done;
+          h->n_items = (int)(it.size() / 4);
+          if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 4) * 4))) goto done;
           if (!it.empty()) CK(cudaMemcpy(h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
         }
-        // sparse tiles (mean live-brick fraction < 0.7, typically porosity <= 0.3
-        // or tube networks) run the warp work list by default: measured +2-5 %
-        // there, -2 % on fuller tiles (profiles/sparse_r01.md)
+        // tiles with mean live-brick fraction < 0.85 (porosity up to ~0.7, tube
+        // networks) run the warp work list by default: measured +1-9 % over the
+        // CTA-per-tile kernels there, -3 % on fuller tiles (profiles/sparse_r01.md)
         const double live_frac = T > 0 ? (double)live / ((double)T * (g.tn / bn)) : 1.0;
-        h->auto_wlist = h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.7;
+        h->auto_wlist = h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.85;
         h->live_frac = live_frac;
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag
         // words; the work list when it is used
         h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4 +
-                        (h->auto_wlist ? (long long)h->n_items * 4 : 0);
+                        (h->auto_wlist ? (long long)h->n_items * 16 : 0);
       }
       h->sm.rank = h->rank;
       {

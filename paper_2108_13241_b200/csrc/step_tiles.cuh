@@ -438,49 +438,34 @@ k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   }
 }
 
-// Warp work list (MODE 5): one warp per group of live bricks of one tile
-// (32 lanes = 4 fp32 bricks), items t * 16 + g from a precomputed list, so no
-// lane idles for a tile's dead bricks or its last partial pass and no CTA
-// slot is held by a nearly empty tile.  The 27 neighbour offsets live in
-// lanes 0-26 and are fetched with shuffles.
+// Warp work list (MODE 5/8): one warp per group of live bricks of one tile
+// (32 lanes = 4 fp32 / 8 fp64 bricks), so no lane idles for a tile's dead
+// bricks or its last partial pass and no CTA slot is held by a nearly empty
+// tile.  Each item is pre-decoded on the host: {tile, brick index per lane
+// group (bytes of words 1-2), uniform bits | count << 8}; the chain to the
+// data loads is item -> (nbr27, slot table, flags) -> data.  The 27
+// neighbour offsets live in lanes 0-26 and are fetched with shuffles.
 template <typename T, int TN, int MINB, bool SEL = false>
 __global__ void __launch_bounds__(256, MINB)
 k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask, const int* __restrict__ items, int n_items,
-               const unsigned long long* __restrict__ lut) {
+               const uint4* __restrict__ items, int n_items, const unsigned long long* __restrict__ lut) {
   const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
-  const int item = __ldg(items + wid);
-  const int t = item >> 4, grp = item & 15;
+  const uint4 it = __ldg(items + wid);
+  const int t = (int)it.x;
   int srel = 0;
   if (lane < 27) {
     const int v = __ldg(nbr27 + 27LL * t + lane);
     srel = v < 0 ? 0 : (v - t) * (Q * TN);
   }
   const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  // live-brick ordinal of this lane -> brick index (128-bit mask, words 0-3)
-  uint32_t m[4];
-  int pre_cnt[4], acc = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    m[q] = __ldg(bmask + 8LL * t + q);
-    pre_cnt[q] = acc;
-    acc += __popc(m[q]);
-  }
-  const int j = (grp << (5 - lbn)) + (lane >> lbn);
-  const bool in = j < acc;
-  int q = 3;
-  if (j < pre_cnt[3]) q = 2;
-  if (j < pre_cnt[2]) q = 1;
-  if (j < pre_cnt[1]) q = 0;
-  const uint32_t mq = q == 0 ? m[0] : (q == 1 ? m[1] : (q == 2 ? m[2] : m[3]));
-  const int pq = q == 0 ? 0 : (q == 1 ? pre_cnt[1] : (q == 2 ? pre_cnt[2] : pre_cnt[3]));
-  const int b = in ? q * 32 + (int)__fns(mq, 0, j - pq + 1) : 0;
+  const int gi = lane >> lbn;  // brick group of this lane
+  const bool in = gi < (int)((it.w >> 8) & 15u);
+  const int b = (int)(((gi < 4 ? it.y : it.z) >> (8 * (gi & 3))) & 255u);
   const int l = (b << lbn) | (lane & (bn - 1));
-  const uint32_t uq = __ldg(bmask + 8LL * t + 4 + (b >> 5));
-  const bool uniform = in && ((uq >> (b & 31)) & 1u);
+  const bool uniform = in && ((it.w >> gi) & 1u);
   const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
   const bool live = flag_type(w) != SOLID;
   const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
@@ -575,5 +560,65 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
       const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
       if (live) tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + off] = f[i];
     }
+  }
+}
+
+// A-A over the warp work list (items as in k_step_tiles_w): same per-node
+// work as k_step_tiles_aa, one warp per group of live bricks.  Any work
+// distribution is race-free under A-A: a node reads and writes only its own
+// slots (L) or the slots F[i][x + c_i] that only it reads (NB).
+template <typename T, int TN, int NB, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
+                  const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om, const uint4* __restrict__ items,
+                  int n_items, const unsigned long long* __restrict__ lut) {
+  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wid >= n_items) return;  // whole warps
+  const uint4 it = __ldg(items + wid);
+  const int t = (int)it.x;
+  int srel = 0;
+  if (NB && lane < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + lane);
+    srel = v < 0 ? 0 : (v - t) * (Q * TN);
+  }
+  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
+  const int gi = lane >> lbn;
+  const bool in = gi < (int)((it.w >> 8) & 15u);
+  const int b = (int)(((gi < 4 ? it.y : it.z) >> (8 * (gi & 3))) & 255u);
+  const int l = (b << lbn) | (lane & (bn - 1));
+  const bool uniform = in && ((it.w >> gi) & 1u);
+  const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
+  const bool live = flag_type(w) != SOLID;
+  T* __restrict__ tb = F + (size_t)t * (Q * TN);
+  if (!NB) {
+    if (!live) return;
+    T f[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
+    bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
+    return;
+  }
+  const uint32_t miss = ~w & kMaskBits;
+  T f[Q];
+  {
+    const TileUpLUT up(lut, l);
+    f[0] = live ? LDA(tb + l) : (T)0;
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      const int off = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
+      f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? i * TN + l : opp(i) * TN + off)) : (T)0;
+    }
+  }
+  bc_collide<T>(f, w, bcv, bcr, om);
+  const int l2 = opaque(l);
+  const TileUpLUT up2(lut, l2);
+  if (live) tb[l2] = f[0];
+#pragma unroll
+  for (int i = 1; i < Q; ++i) {
+    const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
+    if (live) tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + off] = f[i];
   }
 }

@@ -452,8 +452,8 @@ def test_boundary_table_limit_and_bad_descriptors():
 @pytest.mark.parametrize("phi", [0.15, 0.5, 0.95])
 def test_default_tile_kernel_choice_is_bitwise(phi):
     """The tile kernel is picked from the live-brick fraction of the kept
-    tiles (warp work list + select below 0.70, CTA per tile + select below
-    0.85, speculative above); every choice reproduces the oracle bitwise."""
+    tiles (warp work list + select below 0.85, speculative CTA per tile
+    above); every choice reproduces the oracle bitwise."""
     from oracle.step19 import OracleSim
     geom = lb.build_porous_random(64, phi, seed=2, radius_range=(3, 9), dims=(64, 48, 32))
     params = lb.FlowParams.from_viscosity(U=0.05, L=47, nu=0.2)
@@ -465,7 +465,7 @@ def test_default_tile_kernel_choice_is_bitwise(phi):
     bt = b.reshape(nz // 8, 4, ny // 8, 4, nx // 8, 4).sum(axis=(1, 3, 5))
     kept = bt > 0
     live_frac = bt[kept].sum() / (kept.sum() * 64)
-    assert bool(sim.stats().tile_work_list) == (live_frac < 0.7)
+    assert bool(sim.stats().tile_work_list) == (live_frac < 0.85)
     sim.initialize(1.004)
     sim.step(9)
     d = geom.descriptors
