@@ -21,7 +21,9 @@ timeout 1500 python bench.py --workload c5 --steps 300 --warmup 10 --no-cpu > gp
 for W in channel512 porous512; do
   timeout 900 python bench.py --workload $W --dtype f64 --steps 300 --warmup 20 --no-cpu --no-e2e > gpurun_out/bench_${TAG}_${W}_f64.json 2>&1
 done
-timeout 900 python bench.py --workload porous512 --scheme aa --no-cpu --no-e2e > gpurun_out/bench_${TAG}_porous512_aa.json 2>&1
+for W in porous512 vascular1024; do
+  timeout 900 python bench.py --workload $W --scheme aa --no-cpu --no-e2e > gpurun_out/bench_${TAG}_${W}_aa.json 2>&1
+done
 for P in 0.1 0.2 0.3 0.5 0.7 0.9; do
   timeout 600 python bench.py --workload porous512@$P --steps 300 --warmup 20 --no-cpu --no-e2e > gpurun_out/sweep_${TAG}_$P.json 2>&1
 done
