@@ -366,10 +366,10 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
     if (var == 5 || var == 8) {
       constexpr int MW = sizeof(T) == 4 ? 6 : 3;
       if (h->n_items && var == 5)
-        k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
+        k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
             pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
       else if (h->n_items)
-        k_step_tiles_w<T, TN, MW, true><<<(unsigned)((h->n_items + 7) / 8), 256, 0, h->stream>>>(
+        k_step_tiles_w<T, TN, MW, true><<<(unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
             pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
       return;
     }
@@ -407,13 +407,13 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
     const bool wl = h->variant_set ? (h->variant == 5 || h->variant == 8) : h->auto_wlist;
     if (wl) {
       if (!h->n_items) return;
-      const unsigned nb = (unsigned)((h->n_items + 7) / 8);
+      const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
       const uint4* it = (const uint4*)h->items;
       if (h->parity == 0)
-        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 3><<<nb, 256, 0, h->stream>>>(
+        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
             F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
       else
-        k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 256, 0, h->stream>>>(
+        k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
             F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
       return;
     }
@@ -1092,15 +1092,17 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           for (long long t = 0; t < T; ++t) {
             uint32_t rec[4] = {(uint32_t)t, 0u, 0u, 0u};
             int k = 0;
-            for (int b = 0; b < 128; ++b) {
-              if (!((hb[8 * t + (b >> 5)] >> (b & 31)) & 1u)) continue;
-              rec[1 + k / 4] |= (uint32_t)b << (8 * (k & 3));
-              if ((hb[8 * t + 4 + (b >> 5)] >> (b & 31)) & 1u) rec[3] |= 1u << k;
-              if (++k == per) {
-                rec[3] |= (uint32_t)k << 8;
-                it.insert(it.end(), rec, rec + 4);
-                rec[1] = rec[2] = rec[3] = 0u;
-                k = 0;
+            for (int q = 0; q < 4; ++q) {
+              for (uint32_t mq = hb[8 * t + q]; mq; mq &= mq - 1) {
+                const int b = q * 32 + __builtin_ctz(mq);
+                rec[1 + k / 4] |= (uint32_t)b << (8 * (k & 3));
+                if ((hb[8 * t + 4 + q] >> (b & 31)) & 1u) rec[3] |= 1u << k;
+                if (++k == per) {
+                  rec[3] |= (uint32_t)k << 8;
+                  it.insert(it.end(), rec, rec + 4);
+                  rec[1] = rec[2] = rec[3] = 0u;
+                  k = 0;
+                }
               }
             }
             if (k) {

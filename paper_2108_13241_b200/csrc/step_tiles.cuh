@@ -438,6 +438,13 @@ k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   }
 }
 
+#ifndef LBM_WL_WARPS
+#define LBM_WL_WARPS 4
+#endif
+// warps per block of the work-list kernels (MINB is given per 8 warps);
+// 4 measured 0-7 % faster than 8 or 2 (profiles/ab_warps_per_block_r01.txt)
+constexpr int kWarpsPerBlock = LBM_WL_WARPS;
+
 // Warp work list (MODE 5/8): one warp per group of live bricks of one tile
 // (32 lanes = 4 fp32 / 8 fp64 bricks), so no lane idles for a tile's dead
 // bricks or its last partial pass and no CTA slot is held by a nearly empty
@@ -446,11 +453,11 @@ k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
 // data loads is item -> (nbr27, slot table, flags) -> data.  The 27
 // neighbour offsets live in lanes 0-26 and are fetched with shuffles.
 template <typename T, int TN, int MINB, bool SEL = false>
-__global__ void __launch_bounds__(256, MINB)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
 k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
                const uint4* __restrict__ items, int n_items, const unsigned long long* __restrict__ lut) {
-  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
   const uint4 it = __ldg(items + wid);
@@ -568,11 +575,11 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
 // distribution is race-free under A-A: a node reads and writes only its own
 // slots (L) or the slots F[i][x + c_i] that only it reads (NB).
 template <typename T, int TN, int NB, int MINB>
-__global__ void __launch_bounds__(256, MINB)
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
 k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                   const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om, const uint4* __restrict__ items,
                   int n_items, const unsigned long long* __restrict__ lut) {
-  const int wid = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
   const uint4 it = __ldg(items + wid);
