@@ -1089,7 +1089,13 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           const int per = 32 / bn;  // 4 (fp32 2x2x2 bricks) or 8 (fp64 2x2x1)
           std::vector<uint32_t> it;
           it.reserve((size_t)(live / per + T) * 4);
-          for (long long t = 0; t < T; ++t) {
+          std::vector<int> ho;  // LBM_TILE_ORDER also orders the work list
+          if (h->order && T > 0) {
+            ho.resize(T);
+            CK(cudaMemcpy(ho.data(), h->order, T * 4, cudaMemcpyDeviceToHost));
+          }
+          for (long long k2 = 0; k2 < T; ++k2) {
+            const long long t = ho.empty() ? k2 : ho[k2];
             uint32_t rec[4] = {(uint32_t)t, 0u, 0u, 0u};
             int k = 0;
             for (int q = 0; q < 4; ++q) {
