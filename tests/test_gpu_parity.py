@@ -354,6 +354,8 @@ def test_launch_configuration_does_not_change_results(monkeypatch):
         assert np.array_equal(run("pointer_tile", LBM_STEP_VARIANT=v), ref), v
     for order in ("morton", "pencil:2", "z:2"):
         assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order), ref), order
+        # the work list follows the launch order too
+        assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order, LBM_STEP_VARIANT="8"), ref), order
     for tile in ((4, 8, 16), (16, 4, 8), (8, 4, 1)):
         assert np.array_equal(run("pointer_tile", tile=tile), ref), tile
 
