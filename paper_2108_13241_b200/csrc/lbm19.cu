@@ -409,8 +409,11 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
       if (!h->n_items) return;
       const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
       const uint4* it = (const uint4*)h->items;
+      // 48 resident warps for both phases (40 registers; the neighbour step
+      // spills 8 B and still measured 0-1 % faster than 40 warps at 48
+      // registers, profiles/ab_aa_warp_list_r01.txt)
       if (h->parity == 0)
-        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
+        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
             F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
       else
         k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
