@@ -103,6 +103,7 @@ struct lbm_handle {
   unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
   int n_items = 0;
   bool auto_wlist = false;  // default tile kernel = warp work list (sparse tiles)
+  bool wlist_ok = false;    // work-list items fit their packing (<= 8 brick groups per warp)
   double live_frac = 1.0;   // live bricks / brick slots of the kept tiles
   bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
   int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows, 3 z-groups of `pencil` layers
@@ -187,6 +188,15 @@ void dev_free(void* p) {
   if (p) cudaFree(p);
 }
 
+// Copies of state the solver stream touches go through that stream: the
+// legacy default stream does not order against a non-blocking stream, and a
+// pageable cudaMemcpy can return before its DMA has landed.
+cudaError_t scopy(const lbm_handle* h, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  return e;
+}
+
 void drop_graphs(lbm_handle* h) {
   for (int p = 0; p < 2; ++p)
     if (h->graph[p]) {
@@ -209,6 +219,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->lut);
   h->lut = nullptr;
   h->n_items = 0;
+  h->wlist_ok = h->auto_wlist = false;
   dev_free(h->gh[0]);
   dev_free(h->gh[1]);
   h->gh[0] = h->gh[1] = nullptr;
@@ -330,6 +341,7 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
   // < 0.85 warp work list + exact per-link select (8); fuller tiles the
   // speculative CTA-per-tile kernel (7)
   if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : 7;
+  if ((var == 5 || var == 8) && !h->wlist_ok) var = 7;
   if (TH.on) {  // z-slab: a live-brick kernel with the ghost-plane exchange
     if constexpr (TN == 512) {
       k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true><<<nt, BT, 0, h->stream>>>(
@@ -404,7 +416,7 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
   constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap (48)
   if constexpr (TN == 512) {
     // the warp work list where the AB step would use it (or when variant 5/8 is forced)
-    const bool wl = h->variant_set ? (h->variant == 5 || h->variant == 8) : h->auto_wlist;
+    const bool wl = h->wlist_ok && (h->variant_set ? (h->variant == 5 || h->variant == 8) : h->auto_wlist);
     if (wl) {
       if (!h->n_items) return;
       const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
@@ -920,6 +932,9 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
   if (!h || !type || !orient || !bc_index) return fail(LBM_EINVAL, "NULL geometry array");
   if (nb < 0 || nb > 255) return fail(LBM_EINVAL, "boundary table holds %d entries; at most 255 supported", nb);
   if (nb > 0 && (!bc_kind || !bc_vel || !bc_rho)) return fail(LBM_EINVAL, "NULL boundary table");
+  if (h->lo.on || h->hi.on)
+    return fail(LBM_ESTATE, "z-slab is connected to its neighbours (they map its buffers): "
+                            "destroy the slab handles instead of replacing the geometry");
   DeviceGuard dg(h->d.device);
   CK(cudaStreamSynchronize(h->stream));
   free_geometry(h);
@@ -944,6 +959,8 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     goto done;
   CK(cudaMemsetAsync(derr, 0, 16, h->stream));
   CK(cudaMemsetAsync(h->uscratch, 0, 4 * sizeof(unsigned long long), h->stream));
+  h->has_glo = ghost_lo != nullptr;  // z-slab: links cross z = -1 / z = nz into a neighbour
+  h->has_ghi = ghost_hi != nullptr;
   if (ghost_lo) {
     if ((rc = dev_alloc(h, &dglo, plane_nodes))) goto done;
     CK(cudaMemcpyAsync(dglo, ghost_lo, plane_nodes, cudaMemcpyHostToDevice, h->stream));
@@ -971,18 +988,18 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         for (int c = 0; c < 3; ++c) vv[3 * b + c] = bc_vel[3 * b + c];
         rr[b] = bc_rho[b];
       }
-      CK(cudaMemcpy(h->bckind64, kk.data(), nbt, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(h->bcv64, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(h->bcr64, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
+      CK(scopy(h, h->bckind64, kk.data(), nbt, cudaMemcpyHostToDevice));
+      CK(scopy(h, h->bcv64, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
+      CK(scopy(h, h->bcr64, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
       if (h->esize == 4) {
         std::vector<float> vf(nbt * 3), rf(nbt);
         for (int k = 0; k < nbt * 3; ++k) vf[k] = (float)vv[k];
         for (int k = 0; k < nbt; ++k) rf[k] = (float)rr[k];
-        CK(cudaMemcpy(h->bcv, vf.data(), nbt * 3 * 4, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->bcr, rf.data(), nbt * 4, cudaMemcpyHostToDevice));
+        CK(scopy(h, h->bcv, vf.data(), nbt * 3 * 4, cudaMemcpyHostToDevice));
+        CK(scopy(h, h->bcr, rf.data(), nbt * 4, cudaMemcpyHostToDevice));
       } else {
-        CK(cudaMemcpy(h->bcv, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(h->bcr, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
+        CK(scopy(h, h->bcv, vv.data(), nbt * 3 * 8, cudaMemcpyHostToDevice));
+        CK(scopy(h, h->bcr, rr.data(), nbt * 8, cudaMemcpyHostToDevice));
       }
     }
     if (!g.tiled) {
@@ -1090,14 +1107,18 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         // after one dependent load instead of walking the brick masks
         {
           const int per = 32 / bn;  // 4 (fp32 2x2x2 bricks) or 8 (fp64 2x2x1)
+          // an item packs at most 8 brick bytes and a 4-bit count; smaller
+          // bricks (LBM_BRICK=0 with a tile x-edge under one sector) run the
+          // CTA-per-tile kernels instead
+          h->wlist_ok = per <= 8;
           std::vector<uint32_t> it;
           it.reserve((size_t)(live / per + T) * 4);
           std::vector<int> ho;  // LBM_TILE_ORDER also orders the work list
           if (h->order && T > 0) {
             ho.resize(T);
-            CK(cudaMemcpy(ho.data(), h->order, T * 4, cudaMemcpyDeviceToHost));
+            CK(scopy(h, ho.data(), h->order, T * 4, cudaMemcpyDeviceToHost));
           }
-          for (long long k2 = 0; k2 < T; ++k2) {
+          for (long long k2 = 0; h->wlist_ok && k2 < T; ++k2) {
             const long long t = ho.empty() ? k2 : ho[k2];
             uint32_t rec[4] = {(uint32_t)t, 0u, 0u, 0u};
             int k = 0;
@@ -1122,13 +1143,13 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           pt.mark("brick masks to host + work list");
           h->n_items = (int)(it.size() / 4);
           if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 4) * 4))) goto done;
-          if (!it.empty()) CK(cudaMemcpy(h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
+          if (!it.empty()) CK(scopy(h, h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
         }
         // tiles with mean live-brick fraction < 0.85 (porosity up to ~0.7, tube
         // networks) run the warp work list by default: measured +1-9 % over the
         // CTA-per-tile kernels there, -3 % on fuller tiles (profiles/sparse_r01.md)
         const double live_frac = T > 0 ? (double)live / ((double)T * (g.tn / bn)) : 1.0;
-        h->auto_wlist = h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.85;
+        h->auto_wlist = h->wlist_ok && h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.85;
         h->live_frac = live_frac;
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag
         // words; the work list when it is used
@@ -1157,11 +1178,9 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           lt[l] = w;
         }
         if ((rc = dev_alloc(h, &h->lut, lt.size() * 8))) goto done;
-        CK(cudaMemcpy(h->lut, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice));
+        CK(scopy(h, h->lut, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice));
       }
       // z-slab ghost planes (tile layouts keep them outside the tile storage)
-      h->has_glo = ghost_lo != nullptr;
-      h->has_ghi = ghost_hi != nullptr;
       if (h->has_glo || h->has_ghi) {
         const size_t gb = (size_t)10 * plane_nodes * h->esize;
         if ((rc = dev_alloc(h, (char**)&h->gh[0], gb)) || (rc = dev_alloc(h, (char**)&h->gh[1], gb))) goto done;
@@ -1281,6 +1300,9 @@ int lbm_step_async(lbm_t* h, int64_t n) {
   NvtxRange nv("lbm_step");
   if (n < 0) return fail(LBM_EINVAL, "n_steps must be >= 0, got %lld", (long long)n);
   if (!h->initialized) return fail(LBM_ESTATE, "initialize() must run before stepping");
+  if (n > 0 && ((h->has_glo && !h->lo.on) || (h->has_ghi && !h->hi.on)))
+    return fail(LBM_ESTATE, "z-slab has a ghost plane on its %s side but no neighbour is connected "
+                            "(lbm_halo_connect)", (h->has_glo && !h->lo.on) ? "lower" : "upper");
   DeviceGuard dg(h->d.device);
   const bool halo = halo_on(h);
   if (halo && h->halo_dirty && n > 0) {
@@ -1355,7 +1377,7 @@ int lbm_synchronize(lbm_t* h) {
   h->last_ms = ms;
   if (halo_on(h)) {
     int herr = 0;
-    CK(cudaMemcpy(&herr, h->herr, 4, cudaMemcpyDeviceToHost));
+    CK(scopy(h, &herr, h->herr, 4, cudaMemcpyDeviceToHost));
     if (herr) return fail(LBM_ENCCL, "halo wait timed out: a neighbouring slab stopped stepping");
   }
   return 0;
@@ -1486,7 +1508,7 @@ int lbm_check_finite(lbm_t* h, int32_t* dir, int32_t* node_xyz) {
     const long long t = v / g.tn;
     const int l = (int)(v % g.tn);
     int tc[3];
-    CK(cudaMemcpy(tc, h->tiles + 3 * t, 12, cudaMemcpyDeviceToHost));
+    CK(scopy(h, tc, h->tiles + 3 * t, 12, cudaMemcpyDeviceToHost));
     int lx, ly, lz;
     brick_inv(g, l, lx, ly, lz);
     x = tc[0] * g.ex + lx;
@@ -1644,9 +1666,9 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
   }
   void* buf = h->f[which == 0 ? h->parity : 1 - h->parity];
   if (get)
-    CK(cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost));
+    CK(scopy(h, host, buf, bytes, cudaMemcpyDeviceToHost));
   else
-    CK(cudaMemcpy(buf, host, bytes, cudaMemcpyHostToDevice));
+    CK(scopy(h, buf, host, bytes, cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -1695,8 +1717,8 @@ int lbm_get_tile_index(lbm_t* h, int32_t* tiles, int32_t* nbr27, int64_t* n_tile
   if (n_tiles) *n_tiles = h->n_tiles;
   if (!h->g.tiled) return 0;
   DeviceGuard dg(h->d.device);
-  if (tiles && h->n_tiles) CK(cudaMemcpy(tiles, h->tiles, h->n_tiles * 12, cudaMemcpyDeviceToHost));
-  if (nbr27 && h->n_tiles) CK(cudaMemcpy(nbr27, h->nbr27, h->n_tiles * 27 * 4, cudaMemcpyDeviceToHost));
+  if (tiles && h->n_tiles) CK(scopy(h, tiles, h->tiles, h->n_tiles * 12, cudaMemcpyDeviceToHost));
+  if (nbr27 && h->n_tiles) CK(scopy(h, nbr27, h->nbr27, h->n_tiles * 27 * 4, cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -1720,8 +1742,9 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
   s->scheme = h->d.scheme;
-  s->tile_work_list =
-      (h->auto_wlist && !h->variant_set) || (h->g.tiled && (h->variant == 5 || h->variant == 8)) ? 1 : 0;
+  // z-slab tile handles (ghost planes) run the CTA-per-tile exchange kernel
+  s->tile_work_list = h->gh[0] == nullptr && h->wlist_ok &&
+      ((h->auto_wlist && !h->variant_set) || (h->g.tiled && (h->variant == 5 || h->variant == 8))) ? 1 : 0;
   return 0;
 }
 

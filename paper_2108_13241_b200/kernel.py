@@ -141,6 +141,7 @@ class DeviceField:
     def __init__(self, sim):
         self._sim = sim
         self._mirror = {}
+        self._touched = False   # a writable mirror was handed out (pre/post/write)
         self._slot_of = None
         self.frozen = False
 
@@ -202,12 +203,14 @@ class DeviceField:
 
     @property
     def pre(self):
+        self._touched = True
         return self._get(0)
 
     @property
     def post(self):
         if self._sim.scheme == "aa":
             raise AttributeError("the AA scheme updates one buffer in place: there is no post buffer")
+        self._touched = True
         return self._get(1)
 
     @property
@@ -220,7 +223,11 @@ class DeviceField:
         return self._slot_of
 
     def flush(self):
-        """Write mirrored host edits back to the device and drop the mirrors."""
+        """Write mirrored host edits back to the device and drop the mirrors.
+        Mirrors only downloaded for a read-only view (run() observers) are
+        dropped without an upload."""
+        if not self._touched:
+            self._mirror = {}
         if not self._mirror:
             return
         h = self._sim._handle
@@ -233,9 +240,11 @@ class DeviceField:
                 raw = np.ascontiguousarray(view)
             _lib.check(h.lib.lbm_set_field(h.h, which, _lib.ptr(raw)))
         self._mirror = {}
+        self._touched = False
 
     def invalidate(self):
         self._mirror = {}
+        self._touched = False
 
     def _slot_checked(self, x, y, z, i):
         nx, ny, nz = self.dims
@@ -249,7 +258,9 @@ class DeviceField:
         s = self._slot_checked(x, y, z, i)
         if s < 0:
             return self.dtype.type(0.0)
-        return (self.pre if which == "pre" else self.post)[i, s]
+        if which != "pre" and self._sim.scheme == "aa":
+            raise AttributeError("the AA scheme updates one buffer in place: there is no post buffer")
+        return self._get(0 if which == "pre" else 1)[i, s]  # read: no upload needed
 
     def write(self, x, y, z, i, which, value):
         s = self._slot_checked(x, y, z, i)
@@ -387,7 +398,7 @@ class Simulation:
                 if sc % every_k == 0:
                     if fields is None:
                         fields = self.macroscopic_fields()
-                        view = self.field.pre.view()
+                        view = self.field._get(0).view()  # read-only: no upload after
                         view.setflags(write=False)
                     try:
                         callback(sc, fields, view)

@@ -25,6 +25,14 @@ Cases (reference call sites in brackets):
                    [test_kernel.py:235-245]
 plus the Ghia (1982) Re = 100 centreline table the reference ships
 (pkg/src/sparselbm/data/ghia1982_reference.txt) for the physics check.
+
+Pointer-tile index fixtures (`tiles_<case>.npz`, `python make_golden.py
+--tiles`): the reference's own `layouts.allocate(..., "pointer_tile", ...)`
+tile rank grid (compacted row-major rank of tiles holding >= 1 non-solid
+node, -1 = not allocated; pkg/src/sparselbm/layouts.py:389-401) and its
+slot_of map (rank * 256 + row-major intra-tile index, :263-269, 396-399),
+plus the fully allocated `tile` layout's slot_of, for porous64 and the
+mixed-BC seeds 1-3.
 """
 
 import os
@@ -87,6 +95,31 @@ def record(slb, name, geom, nu, steps, scalar=np.float64, rho0=1.0, v0=(0.0, 0.0
           out["mass_final"])
 
 
+def record_tiles(slb, name, geom):
+    from sparselbm import layouts as L
+    d = geom.descriptors
+    pt = L.allocate(geom.dims, "pointer_tile", np.float64, d.type_tag)
+    full = L.allocate(geom.dims, "tile", np.float64, d.type_tag)
+    out = dict(types=d.type_tag, tile_edge=np.int64(L.TILE_EDGE),
+               tile_rank=pt._tile_rank, slot_of=pt.slot_of,
+               allocated_tiles=np.int64(pt.allocated_tiles),
+               n_slots=np.int64(pt.n_slots), tile_slot_of=full.slot_of)
+    np.savez_compressed(os.path.join(HERE, f"tiles_{name}.npz"), **out)
+    print("tiles", name, geom.dims, "allocated", pt.allocated_tiles, "of",
+          full.allocated_tiles)
+
+
+def main_tiles():
+    slb, refconf = _import_reference()
+    for seed in (1, 2, 3):
+        record_tiles(slb, f"mixed_s{seed}", refconf.random_mixed_geometry(seed))
+    record_tiles(slb, "porous64", slb.build_porous_random(64, 0.6, seed=9))
+    # sparse enough that some 16x16 tiles are all solid (dropped)
+    record_tiles(slb, "porous96_lo", slb.build_porous_random(96, 0.35, seed=4))
+    # 72 = 4.5 tiles: padded edge tiles
+    record_tiles(slb, "porous72_lo", slb.build_porous_random(72, 0.3, seed=5))
+
+
 def main():
     slb, refconf = _import_reference()
     for seed in (1, 2, 3):
@@ -120,4 +153,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--tiles" in sys.argv:
+        main_tiles()
+    else:
+        main()
