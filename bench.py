@@ -14,8 +14,13 @@ One JSON line on rank 0 (contract in the task statement):
   cpu_baseline  the CPU oracle (Numba port of the reference kernel) on the
          host cores, bounded sample of the same workload.
 --impl reference times that CPU implementation alone (the reference arm).
-N > 1 (torchrun): z-slab decomposition of a 1024x1024x(256 N) duct, one rank
-per GPU, halo planes exchanged every step (weak scaling).
+N = 1 default: C2 (dense channel 512^3), plus a `sparse` block with C3
+(porous 512^3 at phi ~0.5 and ~0.1) and C4 (vascular 1024^3) measured in the
+same run.
+N > 1 (torchrun): z-slab decomposition of the C5 duct 1024x1024x(256 N), one
+rank per GPU, halo planes exchanged inside the step kernel (weak scaling;
+N = 8 is the full 1024x1024x2048 domain); rank 0 also reports its slab's
+solo rate (bench_multi.py).
 """
 
 import argparse
@@ -47,16 +52,76 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
-    """Per-launch DRAM bytes of the step kernel from the committed ncu
-    capture (profiles/ncu_summary.json), or None."""
+def expected_kernel(layout, scheme, dtype, tile_work_list):
+    """Name prefix of the step kernel the library launches for this
+    configuration (csrc/lbm19.cu launch_step / launch_tiles)."""
+    t = "float" if dtype == "f32" else "double"
+    if layout in ("tile", "pointer_tile"):
+        if scheme == "aa":
+            return f"k_step_tiles_aa_w<{t}" if tile_work_list else f"k_step_tiles_aa<{t}"
+        return f"k_step_tiles_w<{t}" if tile_work_list else f"k_step_tiles_x<{t}"
+    return f"k_step_dense_aa<{t}" if scheme == "aa" else f"k_step_dense<{t}"
+
+
+def ncu_traffic(workload, dtype, scheme, tile, kernel_prefix):
+    """Per-launch DRAM bytes (read + write) of the step kernel from a
+    committed `ncu --set full` capture of the SAME configuration
+    (profiles/ncu_summary.json entries keyed by workload, dtype, scheme,
+    tile and kernel), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
-            d = json.load(fh)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+            entries = json.load(fh)["entries"]
     except Exception:
         return None
+    for e in entries:
+        if (e.get("workload") == workload and e.get("dtype") == dtype and e.get("scheme") == scheme
+                and (e.get("tile") or None) == (list(tile) if tile else None)
+                and str(e.get("kernel", "")).replace("void ", "").startswith(kernel_prefix)):
+            return e.get("dram_bytes_per_launch")
+    return None
+
+
+def measure_device(lb, workload, geom, params, layout, scheme, tile, dtype, rho0, device, steps,
+                   warmup):
+    """Device-timed K steps (inputs resident in HBM, CUDA events on the
+    solver stream) with the roofline figures of the step kernel."""
+    scalar = np.float32 if dtype == "f32" else np.float64
+    esz = np.dtype(scalar).itemsize
+    sim = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=device, scheme=scheme,
+                        tile=tile)
+    sim.initialize(rho0)
+    sim.step(warmup)
+    launches0 = sim.launches_total
+    with ClockSampler(device) as clk:
+        sim.step(steps)    # CUDA events on the solver stream around K launches
+    ms = sim.last_step_ms
+    launches = sim.launches_total - launches0
+    clocks = clk.summary()
+    nons = sim.active_node_count
+    st = sim.stats()
+    mlups = nons * steps / (ms / 1e3) / 1e6
+    peak, _ = measured_peak()
+    per_launch_ms = ms / launches
+    # algorithmic bytes per launch: 19 reads + 19 writes per non-solid node,
+    # plus the flag / index bytes this design's step reads (dense: flag words
+    # of non-uniform warp chunks + the uniform-chunk bitmap; tiles: nbr27 +
+    # brick masks + flag words of live bricks + the work list)
+    alg_bytes = nons * 2 * 19 * esz + int(st.meta_bytes_per_step)
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+    sane = bool(np.isfinite(sim.total_mass()))
+    tiled = layout in ("tile", "pointer_tile")
+    kern = expected_kernel(layout, scheme, dtype, bool(st.tile_work_list))
+    sim.close()
+    del sim
+    return {"value": mlups, "unit": "MLUPS", "mlups": mlups, "frac": achieved / peak,
+            "achieved_gbs": achieved, "ms": ms, "ms_per_step": ms / steps,
+            "per_launch_ms": per_launch_ms, "alg_bytes": alg_bytes, "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_per_node": alg_bytes / nons, "nons": nons, "non_solid_nodes": int(nons),
+            "porosity": nons / float(st.n_nodes), "stats": st, "launches": launches,
+            "gpu_launches": int(launches), "clocks": clocks, "finite": sane, "kernel": kern,
+            "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile") if tiled else None),
+            "traffic": ncu_traffic(workload, dtype, scheme, tile if tiled else None, kern)}
 
 
 def build_workload(name, rank=0, world=1):
@@ -158,78 +223,58 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_baseline(workload_name, target_node_updates=1.0e9, steps=None):
-    """Time the CPU oracle (Numba restatement of the reference kernel,
-    oracle/step19.py) on a bounded sample: a z-slab of the same workload."""
-    import numba
-
-    from oracle.step19 import OracleSim
-    cores = len(os.sched_getaffinity(0))
-    numba.set_num_threads(cores)
-    import paper_2108_13241_b200 as lb
-    if workload_name in ("channel512", "duct"):
-        nzs = 16
-        geom = lb.build_channel(512, 512, nzs, lb.VelocityInlet((0.05, 0.0, 0.0)))
-        omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25).omega
-        sample = f"512x512x{nzs} z-periodic slab of the C2 channel (same per-node work), fp32"
-        rho0 = 1.0
-    else:
-        geom = lb.build_porous_random(512, 0.5, seed=0, radius_range=(4, 32), dims=(512, 512, 16))
-        omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.5).omega
-        sample = "512x512x16 slab porous geometry, fp32"
-        rho0 = 1.008
-    d = geom.descriptors
-    kinds, vel, rho = geom.boundary_values.as_arrays()
-    sim = OracleSim(d.type_tag, d.orientation, d.bc_index, kinds, vel, rho, omega,
-                    dtype=np.float32, periodic=d.periodic)
-    sim.initialize(rho0)
-    sim.step(1)   # JIT
-    nons = int(np.count_nonzero(d.type_tag))
-    if steps is None:
-        steps = max(3, int(target_node_updates / nons / 5))
-    # best of five samples: the GPU box's host is shared and the port's rate
-    # swings between ~50 and ~88 MLUPS over periods of seconds
-    # (profiles/cpu_baseline_check.py)
-    rates = []
-    for _ in range(5):
-        t0 = time.perf_counter()
-        sim.step(steps)
-        rates.append(nons * steps / (time.perf_counter() - t0) / 1e6)
-    return {"value": max(rates), "unit": "MLUPS", "cores": cores, "kind": "port",
-            "sample": f"{sample}, best of 5 x {steps} steps ({nons * steps / 1e6:.0f} M node updates each; "
-                      f"MLUPS {', '.join(f'{r:.1f}' for r in rates)}), "
-                      "Numba parallel over rows, numba threads = cores"}
+CPU_SLAB_NZ = 32   # the CPU sample: 512 x 512 x 32 z-periodic slab of C2
 
 
-def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    # each timed step = one CPU oracle step on the sample slab
+def _cpu_port_sim():
     import numba
 
     from oracle.step19 import OracleSim
     import paper_2108_13241_b200 as lb
     cores = len(os.sched_getaffinity(0))
     numba.set_num_threads(cores)
-    # ~1 minute of CPU work for the whole timed run (LBM_REF_BUDGET: node updates)
-    budget_updates = float(os.environ.get("LBM_REF_BUDGET", "2.0e9"))
-    nzs = int(max(1, min(512, round(budget_updates / (args.steps * 512 * 512)))))
-    geom = lb.build_channel(512, 512, nzs, lb.VelocityInlet((0.05, 0.0, 0.0)))
+    geom = lb.build_channel(512, 512, CPU_SLAB_NZ, lb.VelocityInlet((0.05, 0.0, 0.0)))
     omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25).omega
     d = geom.descriptors
     kinds, vel, rho = geom.boundary_values.as_arrays()
     sim = OracleSim(d.type_tag, d.orientation, d.bc_index, kinds, vel, rho, omega,
                     dtype=np.float32, periodic=d.periodic)
     sim.initialize(1.0)
+    return sim, int(np.count_nonzero(d.type_tag)), cores
+
+
+def _cpu_protocol(steps, warmup):
+    return (f"one protocol for both arms: 512x512x{CPU_SLAB_NZ} z-periodic slab of the C2 channel "
+            f"(same per-node work as C2), fp32, Numba port of the reference kernel (oracle/step19.py) "
+            f"parallel over rows with numba threads = host cores; {warmup} warm-up step(s) (JIT), then "
+            f"{steps} steps timed as one continuous wall-clock region")
+
+
+def cpu_baseline(workload_name, steps=190):
+    """The reference's CPU path (the Numba port, oracle/step19.py) on the host
+    cores: a bounded ~20 s sample of C2-type work, the same protocol as the
+    --impl reference arm (only the step count differs)."""
+    sim, nons, cores = _cpu_port_sim()
+    sim.step(1)   # JIT
+    t0 = time.perf_counter()
+    sim.step(steps)
+    v = nons * steps / (time.perf_counter() - t0) / 1e6
+    return {"value": v, "unit": "MLUPS", "cores": cores, "kind": "port",
+            "sample": _cpu_protocol(steps, 1) + f" ({nons * steps / 1e6:.0f} M node updates)"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # each timed step = one step of the CPU port on the sample slab
+    sim, nons, cores = _cpu_port_sim()
     sim.step(max(args.warmup, 1))
-    nons = int(np.count_nonzero(d.type_tag))
     t0 = time.perf_counter()
     sim.step(args.steps)
     dt = time.perf_counter() - t0
     v = nons * args.steps / dt / 1e6
-    sample = (f"512x512x{nzs} z-periodic slab of the C2 channel per step "
-              "(same per-node work), fp32, Numba port of the reference kernel")
+    sample = _cpu_protocol(args.steps, max(args.warmup, 1))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "MLUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
@@ -258,6 +303,8 @@ def main():
                     help="PDF storage: two buffers (ab) or one in place (aa)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sparse", action="store_true",
+                    help="skip the C3/C4 sparse block of the default (C2) line")
     ap.add_argument("--variants", default=None,
                     help="comma list of step-kernel variants to time in-process (tuning)")
     args = ap.parse_args()
@@ -315,30 +362,12 @@ def main():
                               "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
         return
-    sim = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=local, scheme=scheme,
-                        tile=tile)
-    sim.initialize(rho0)
-    sim.step(args.warmup)
-    launches0 = sim.launches_total
-    with ClockSampler(local) as clk:
-        sim.step(args.steps)    # CUDA events on the solver stream around K launches
-    ms = sim.last_step_ms
-    launches = sim.launches_total - launches0
-    clocks = clk.summary()
-    nons = sim.active_node_count
-    st = sim.stats()
-    mlups = nons * args.steps / (ms / 1e3) / 1e6
+    dev = measure_device(lb, workload, geom, params, layout, scheme, tile, args.dtype, rho0, local,
+                         args.steps, args.warmup)
+    st, nons, ms, launches, clocks = dev["stats"], dev["nons"], dev["ms"], dev["launches"], dev["clocks"]
+    mlups, per_launch_ms = dev["mlups"], dev["per_launch_ms"]
     peak, peak_src = measured_peak()
-    per_launch_ms = ms / launches
-    # algorithmic bytes per launch: 19 reads + 19 writes of fp32 per non-solid
-    # node, plus the flag / index bytes this design's step reads (dense: flag
-    # words of non-uniform warp chunks + the uniform-chunk bitmap; tiles:
-    # nbr27 + brick masks + flag words of live bricks)
-    alg_bytes = nons * 2 * 19 * esz + int(st.meta_bytes_per_step)
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-    sane = bool(np.isfinite(sim.total_mass()))
-    sim.close()
-    del sim
+    alg_bytes, achieved, sane = dev["alg_bytes"], dev["achieved_gbs"], dev["finite"]
 
     e2e = None
     if not args.no_e2e:
@@ -376,6 +405,25 @@ def main():
         copy_gbs = None
 
 
+    # driver-visible sparse configs (C3 at two porosities, C4), measured in
+    # this same run with the same K / W: the >= 70 % sparse target
+    sparse = None
+    if workload == "channel512" and args.dtype == "f32" and not args.no_sparse:
+        sparse = {}
+        for w in ("porous512", "porous512@0.1", "vascular1024"):
+            try:
+                g2, p2, l2, d2, r2 = build_workload(w)
+                m = measure_device(lb, w, g2, p2, l2, DEFAULT_SCHEME, tile, args.dtype, r2, local,
+                                   args.steps, args.warmup)
+                sparse[w] = {k: m[k] for k in ("value", "unit", "frac", "achieved_gbs", "ms_per_step",
+                                               "alg_bytes_per_launch", "alg_bytes_per_node",
+                                               "traffic", "non_solid_nodes", "porosity", "tile_kernel",
+                                               "gpu_launches", "clocks")}
+                sparse[w]["workload"] = d2
+                del g2
+            except Exception as exc:  # reported, never fatal for the headline
+                sparse[w] = {"error": repr(exc)}
+
     line = {
         "metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -390,7 +438,7 @@ def main():
                    "parallelism": "single GPU"},
         "mlups_per_gpu": mlups,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(workload),
+                     "frac": achieved / peak, "traffic": dev["traffic"],
                      "peak_source": peak_src,
                      "alg_bytes_per_launch": alg_bytes,
                      "alg_bytes_per_node": alg_bytes / nons,
@@ -402,6 +450,8 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "finite": sane,
     }
+    if sparse is not None:
+        line["sparse"] = sparse
     print(json.dumps(line), flush=True)
 
 

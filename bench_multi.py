@@ -1,7 +1,12 @@
 """Multi-GPU leg of bench.py (launched by torchrun, one rank per GPU).
 
-Weak scaling of config C2: every rank owns a 512^3 z-slab of a z-periodic
-channel of global extent 512 x 512 x (512 N); ranks form a ring.  The step
+Default: weak scaling of config C5: every rank owns a 1024 x 1024 x 256
+z-slab of the duct 1024 x 1024 x (256 N) (velocity inlet at z = 0, pressure
+outlet at the top; N = 8 is the full 1024 x 1024 x 2048 domain).  Rank 0
+also times its slab geometry ALONE on its GPU (no neighbours) after the
+multi-rank run, so the line carries the per-GPU solo rate the weak-scaling
+efficiency is measured against.  --workload channel512 runs the C2 ring
+(512^3 per rank, z-periodic), --workload c5 the strong-scaling split.  The step
 kernel stores the outgoing c_z = +-1 populations of its two boundary planes
 straight into the neighbours' ghost planes (CUDA IPC peer memory over
 NVLink), device flags order the steps.  Timing: barrier + synchronize, K
@@ -34,7 +39,7 @@ def run_multi(args, rank, world, local):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dev = "cuda"
-    workload = args.workload or "channel512"
+    workload = args.workload or "duct"
     scaling = "weak"
     if workload == "c5":
         # strong scaling of the whole C5 domain: 2048 / N planes per GPU (AB
@@ -47,7 +52,7 @@ def run_multi(args, rank, world, local):
                 f"1024x1024x{2048 // world}, velocity inlet / pressure outlet, fp32")
         periodic = False
         scaling = "strong"
-    elif workload == "duct":
+    elif workload in ("duct", "c5weak"):
         geom, spec = duct_slab(1024, 1024, 256, rank, world)
         params = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1)
         desc = (f"C5: D3Q19 duct 1024x1024x{256 * world} along z, z-slabs of 1024x1024x256 per "
@@ -135,7 +140,28 @@ def run_multi(args, rank, world, local):
     d2h = sum(a.nbytes for a in fields)
     del fields
     s2.close()
+    # rank 0: the same slab geometry alone on its GPU (no halo), same K / W
+    solo = None
+    dist.barrier()
+    if rank == 0 and workload != "c5":
+        if workload == "channel512":
+            g1 = lb.build_channel(512, 512, 512, lb.VelocityInlet((0.05, 0.0, 0.0)))
+        else:
+            g1 = lb.build_duct_z(1024, 1024, 256)
+        s1 = lb.Simulation(g1, params, layout="dense", scalar=np.float32, device=local, scheme=scheme)
+        s1.initialize(1.0)
+        s1.step(args.warmup)
+        s1.step(args.steps)
+        solo = {"value": s1.active_node_count * args.steps / (s1.last_step_ms / 1e3) / 1e6,
+                "unit": "MLUPS", "what": "rank 0's slab extent as a standalone domain on its GPU "
+                "(no neighbours), same K / W, CUDA events",
+                "weak_scaling_efficiency": None}
+        solo["weak_scaling_efficiency"] = (mlups / world) / solo["value"]
+        s1.close()
+        del s1, g1
+    dist.barrier()
     if rank == 0:
+        line["solo_mlups_per_gpu"] = solo
         line["e2e"] = {"value": total_nons * args.steps / float(te[0]) / 1e6, "unit": "MLUPS",
                        "h2d_bytes_per_step": world * h2d / args.steps,
                        "d2h_bytes_per_step": world * d2h / args.steps,

@@ -2,7 +2,10 @@
 profiles/ncu_summary.json (read by bench.py for roofline.traffic) and
 profiles/ncu_<tag>.md.
 
-    python profiles/summarize_ncu.py <tag> [workload ...]
+    python profiles/summarize_ncu.py <tag> [--dtype f32] [--scheme ab] [--tile 4,8,16] [workload ...]
+
+Entries are keyed by (workload, dtype, scheme, tile, kernel): bench.py only
+takes `roofline.traffic` from a capture of the same configuration.
 """
 
 import csv
@@ -62,12 +65,24 @@ def raw(rep):
     return out
 
 
+DENSE = ("channel512", "cavity64", "c5", "duct")
+
+
 def main():
-    tag = sys.argv[1]
-    wls = sys.argv[2:] or ["channel512"]
+    argv = sys.argv[1:]
+    opts = {"--dtype": "f32", "--scheme": "ab", "--tile": "4,8,16"}
+    rest = []
+    while argv:
+        a = argv.pop(0)
+        if a in opts:
+            opts[a] = argv.pop(0)
+        else:
+            rest.append(a)
+    tag, wls = rest[0], rest[1:] or ["channel512"]
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    summary = json.load(open(path)) if os.path.exists(path) else {}
-    md = [f"# ncu summary `{tag}` (`--set full --clock-control none`, one step-kernel launch)\n",
+    entries = json.load(open(path)).get("entries", []) if os.path.exists(path) else []
+    md = [f"# ncu summary `{tag}` (`--set full --clock-control none`, one step-kernel launch; "
+          f"{opts['--dtype']}, scheme {opts['--scheme']})\n",
           "| workload | kernel | ms | DRAM read GB | DRAM write GB | regs | warps active % | "
           "issue active % | L2 hit % | tensor pipe % |", "|---|---|---|---|---|---|---|---|---|---|"]
     for w in wls:
@@ -78,19 +93,23 @@ def main():
             continue
         k = raw(rep)[0]
         traffic = k["dram_read"] + k["dram_write"]
-        summary[w] = {"tag": tag, "kernel": k["kernel"].split("(")[0],
-                      "duration_ms": k["duration"] * 1e3, "dram_bytes_per_launch": traffic,
-                      "dram_read": k["dram_read"], "dram_write": k["dram_write"],
-                      "registers": k.get("registers"), "warps_active_pct": k.get("warps_active_pct"),
-                      "issue_active_pct": k.get("issue_active_pct"), "l2_hit_pct": k.get("l2_hit_pct"),
-                      "tensor_pipe_pct": k.get("tensor_pipe_pct"),
-                      "stall_long_scoreboard": k.get("stall_long_scoreboard")}
-        md.append(f"| {w} | `{summary[w]['kernel']}` | {k['duration'] * 1e3:.3f} | "
+        tile = None if w.split("@")[0] in DENSE else [int(v) for v in opts["--tile"].split(",")]
+        e = {"workload": w, "dtype": opts["--dtype"], "scheme": opts["--scheme"], "tile": tile,
+             "tag": tag, "kernel": k["kernel"].split("(")[0],
+             "duration_ms": k["duration"] * 1e3, "dram_bytes_per_launch": traffic,
+             "dram_read": k["dram_read"], "dram_write": k["dram_write"],
+             "registers": k.get("registers"), "warps_active_pct": k.get("warps_active_pct"),
+             "issue_active_pct": k.get("issue_active_pct"), "l2_hit_pct": k.get("l2_hit_pct"),
+             "tensor_pipe_pct": k.get("tensor_pipe_pct"),
+             "stall_long_scoreboard": k.get("stall_long_scoreboard")}
+        key = lambda x: (x["workload"], x["dtype"], x["scheme"], x["tile"], x["kernel"])
+        entries = [x for x in entries if key(x) != key(e)] + [e]
+        md.append(f"| {w} | `{e['kernel']}` | {k['duration'] * 1e3:.3f} | "
                   f"{k['dram_read'] / 1e9:.3f} | {k['dram_write'] / 1e9:.3f} | {k.get('registers')} | "
                   f"{k.get('warps_active_pct', 0):.1f} | {k.get('issue_active_pct', 0):.1f} | "
                   f"{k.get('l2_hit_pct', 0):.1f} | {k.get('tensor_pipe_pct', 0) or 0:.1f} |")
     with open(path, "w") as fh:
-        json.dump(summary, fh, indent=1)
+        json.dump({"entries": entries}, fh, indent=1)
     with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as fh:
         fh.write("\n".join(md) + "\n")
     print("\n".join(md))
