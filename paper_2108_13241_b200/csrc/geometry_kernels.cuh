@@ -113,35 +113,6 @@ __global__ void k_tile_nbr(int* __restrict__ nbr, const int* __restrict__ tiles,
   nbr[k] = v;
 }
 
-// Morton key of each kept tile (x, y, z bits interleaved), sorted to a launch
-// order: 3-D neighbours of a tile then run close in time, so the sectors they
-// share (pulled across tile faces, or pushed by the AA neighbour step) are
-// still in L2 when the second CTA touches them.  The rank order itself --
-// the reference's row-major pointer-tile order -- is unchanged.
-__device__ __forceinline__ unsigned long long spread3(unsigned v) {
-  unsigned long long x = v & 0x1fffffu;
-  x = (x | x << 32) & 0x1f00000000ffffULL;
-  x = (x | x << 16) & 0x1f0000ff0000ffULL;
-  x = (x | x << 8) & 0x100f00f00f00f00fULL;
-  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
-  x = (x | x << 2) & 0x1249249249249249ULL;
-  return x;
-}
-// mode 1: Morton; mode 2: y-pencils of B tile rows -- (y block, z, y, x) with
-// x fastest, so a tile's z neighbour runs gx*B tiles later instead of gx*gy
-__global__ void k_tile_order_key(unsigned long long* __restrict__ key, int* __restrict__ val,
-                                 const int* __restrict__ tiles, long long T, int mode, int B, Geo g) {
-  const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= T) return;
-  const unsigned tx = tiles[3 * r], ty = tiles[3 * r + 1], tz = tiles[3 * r + 2];
-  if (mode == 1)
-    key[r] = spread3(tx) | spread3(ty) << 1 | spread3(tz) << 2;
-  else if (mode == 2)
-    key[r] = ((((unsigned long long)(ty / B) * g.gz + tz) * B + ty % B) * g.gx) + tx;
-  else  // mode 3: z-groups of B tile layers interleaved, (tz / B, ty, tx, tz % B)
-    key[r] = ((((unsigned long long)(tz / B) * g.gy + ty) * g.gx + tx) * B) + tz % B;
-  val[r] = (int)r;
-}
 
 // tiles: one thread per slot of the kept tiles
 __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict__ tiles,

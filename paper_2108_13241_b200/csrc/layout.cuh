@@ -46,7 +46,7 @@ __host__ __device__ __forceinline__ void brick_inv(const Geo& g, int l, int& lx,
 
 // element index of (direction i, slot s): dense SoA i*ps + s; tiles AoSoA
 // f[tile][i][node], i.e. each tile's 19 direction blocks are contiguous
-__device__ __forceinline__ long long fidx(const Geo& g, int i, long long s) {
+__host__ __device__ __forceinline__ long long fidx(const Geo& g, int i, long long s) {
   if (!g.tiled) return (long long)i * g.ps + s;
   return ((s >> g.ltn) * Q + i) << g.ltn | (s & (g.tn - 1));
 }

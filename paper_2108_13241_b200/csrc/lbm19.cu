@@ -34,8 +34,10 @@
 #include <chrono>
 #include <cstring>
 #include <unistd.h>
+#include <sys/mman.h>
 #include <string>
 #include <thread>
+#include <sys/mman.h>
 #include <vector>
 
 #include "d3q19.cuh"
@@ -97,7 +99,6 @@ struct lbm_handle {
   int* rank = nullptr;    // tile rank grid
   int* tiles = nullptr;   // (T, 3)
   int* nbr27 = nullptr;   // (T, 27)
-  int* order = nullptr;   // (T) CTA -> tile rank launch order (Morton), or null (rank order)
   void* gh[2] = {nullptr, nullptr};  // tile slabs: ghost planes per buffer, [lo | hi] x 5 x ny x nx
   uint32_t* items = nullptr;  // warp work list, 4 words per warp (tile, brick bytes x2, uniform | count), MODE 5/8
   unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
@@ -106,8 +107,6 @@ struct lbm_handle {
   bool wlist_ok = false;    // work-list items fit their packing (<= 8 brick groups per warp)
   double live_frac = 1.0;   // live bricks / brick slots of the kept tiles
   bool has_glo = false, has_ghi = false;  // tile slabs: links cross z = -1 / z = nz
-  int order_mode = 0;     // 0 rank order, 1 Morton, 2 y-pencils of `pencil` tile rows, 3 z-groups of `pencil` layers
-  int pencil = 4;
   uint32_t* bmask = nullptr;  // (T, 4) live-brick bit masks
   uint32_t* ubits = nullptr;  // dense: uniform-chunk bitmap (1 bit per 32 nodes)
   bool use_ubits = true;
@@ -142,10 +141,10 @@ struct lbm_handle {
   } lo, hi;
   unsigned long long* sync = nullptr;  // [0] written by the lower, [1] by the upper neighbour
   int* herr = nullptr;
-  unsigned long long epoch = 0;        // halo pushes done by this handle
   bool halo_dirty = true;
   bool pending = false;                // lbm_step_async issued, not yet synchronised
   cudaGraphExec_t graph[2] = {nullptr, nullptr};  // kGraphSteps steps from parity 0 / 1
+  long long graph_launches = 0;                    // kernel launches per graph replay
   bool use_graph = true;
 };
 
@@ -213,7 +212,6 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->rank);
   dev_free(h->tiles);
   dev_free(h->nbr27);
-  dev_free(h->order);
   dev_free(h->items);
   h->items = nullptr;
   dev_free(h->lut);
@@ -232,7 +230,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->bcr64);
   h->f[0] = h->f[1] = nullptr;
   h->flags = nullptr;
-  h->rank = h->tiles = h->nbr27 = h->order = nullptr;
+  h->rank = h->tiles = h->nbr27 = nullptr;
   h->bmask = nullptr;
   h->ubits = nullptr;
   h->bcv = h->bcr = nullptr;
@@ -244,12 +242,15 @@ void free_geometry(lbm_handle* h) {
 
 bool is_tiled(int layout) { return layout == LBM_LAYOUT_TILE || layout == LBM_LAYOUT_POINTER_TILE; }
 
+// elements of one PDF buffer: 19 planes of ps (tiles: T tiles x 19 blocks)
+long long buf_elems(const lbm_handle* h) { return (long long)Q * h->g.ps; }
+
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g.nz); }
 
 // peer ghost planes of buffer q (lockstep: every slab is at the same parity)
 template <typename T>
 Halo<T> make_halo(const lbm_handle* h, int q) {
-  Halo<T> H;
+  Halo<T> H{};
   if (h->g.aa) {
     // A-A: the neighbours' boundary planes themselves (lower slab's top plane,
     // upper slab's plane 0) -- the neighbour step reads and writes them directly
@@ -302,16 +303,16 @@ long long visits_per_step(const lbm_handle* h) {
 }
 
 void halo_signal(lbm_handle* h) {
-  h->epoch += 1;
   h->launches += 1;
   k_halo_signal<<<1, 1, 0, h->stream>>>(h->lo.on ? h->lo.sync + 1 : nullptr,
-                                         h->hi.on ? h->hi.sync + 0 : nullptr, h->epoch);
+                                         h->hi.on ? h->hi.sync + 0 : nullptr, h->sync + 2);
 }
 
 void halo_wait(lbm_handle* h) {
   h->launches += 1;
-  k_halo_wait<<<1, 1, 0, h->stream>>>(h->sync, h->lo.on, h->hi.on, h->epoch, h->herr);
+  k_halo_wait<<<1, 1, 0, h->stream>>>(h->sync, h->lo.on, h->hi.on, h->herr);
 }
+
 
 template <typename T>
 void halo_push(lbm_handle* h) {
@@ -328,81 +329,65 @@ void halo_push(lbm_handle* h) {
   k_halo_push<T><<<grid, 128, 0, h->stream>>>((const T*)h->f[h->parity], H, h->g);
 }
 
+// TMA-staged tile kernel (variant 9): AB, whole-domain handles
+bool tma_ok(const lbm_handle* h) { return h->g.tiled && !h->g.aa && h->gh[0] == nullptr; }
+
 template <typename T, int TN>
-void launch_tiles(lbm_handle* h, const T* pre, T* post, int var) {
+void launch_tiles_tma(lbm_handle* h, const T* pre, T* post) {
+  using C = TmaCfg<T, TN>;
+  static int blocks = 0;  // resident CTAs per SM (per instantiation; same device family)
+  static int sms = 0;
+  if (!blocks) {
+    cudaFuncSetAttribute(k_step_tiles_tma<T, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_step_tiles_tma<T, TN>, C::THREADS, C::SMEM);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->d.device);
+    if (blocks < 1) blocks = 1;
+  }
+  long long grid = (long long)blocks * sms;
+  if (grid > h->n_tiles) grid = h->n_tiles;
+  k_step_tiles_tma<T, TN><<<(unsigned)grid, C::THREADS, C::SMEM, h->stream>>>(
+      pre, post, h->flags, h->nbr27, (const T*)h->bcv, (const T*)h->bcr, h->g, (T)h->d.omega, h->bmask,
+      (const ulonglong2*)h->lut, (int)h->n_tiles);
+}
+
+template <typename T, int TN>
+void launch_tiles(lbm_handle* h, const T* pre, T* post) {
   constexpr int BT = TN < 256 ? TN : 256;
   const TileHalo<T> TH = make_tile_halo<T>(h, h->parity, 1 - h->parity);
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
+  constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // select / ghost variants need more registers
+  constexpr int MW = sizeof(T) == 4 ? 6 : 3;          // work list: 48 (fp32) resident warps per SM
   const unsigned nt = (unsigned)h->n_tiles;
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
-  // default kernel choice by live-brick fraction (measured, profiles/sparse_r01.md):
-  // < 0.85 warp work list + exact per-link select (8); fuller tiles the
-  // speculative CTA-per-tile kernel (7)
-  if (var == 0 && !h->variant_set) var = h->auto_wlist ? 8 : 7;
-  if ((var == 5 || var == 8) && !h->wlist_ok) var = 7;
-  if (TH.on) {  // z-slab: a live-brick kernel with the ghost-plane exchange
-    if constexpr (TN == 512) {
-      k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true><<<nt, BT, 0, h->stream>>>(
-          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->lut, TH);
-    } else {
-      k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
-          pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order, TH);
-    }
+  const ulonglong2* lut = (const ulonglong2*)h->lut;
+  // kernel choice by live-brick fraction (measured, profiles/sparse_r01.md):
+  // < 0.85 the warp work list with exact per-link select; fuller tiles one
+  // CTA per tile with speculative gathers + bounce-back fix-up.  z-slabs run
+  // the same kernels with the ghost-plane exchange compiled in.
+  const bool wl = h->wlist_ok && (h->variant_set ? h->variant == 8 : h->auto_wlist);
+  if (h->variant_set && h->variant == 9 && tma_ok(h)) {
+    launch_tiles_tma<T, TN>(h, pre, post);
     return;
   }
-  // measured alternatives (LBM_STEP_VARIANT, profiles/sparse_r01.md), built
-  // for the default 512-node tiles only; other tile sizes run the default
-  if constexpr (TN == 512) {
-    constexpr int MS = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // select variants need more registers
-    if (var == 6) {
-      constexpr int SMEM = Q * TN * (int)sizeof(T);
-      constexpr int MSM = (200 * 1024) / (SMEM + 512) > 0 ? (200 * 1024) / (SMEM + 512) : 1;
-      constexpr int MB = MSM < M ? MSM : M;
-      cudaFuncSetAttribute(k_step_tiles_s<T, TN, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      k_step_tiles_s<T, TN, MB><<<nt, BT, SMEM, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                             h->bmask);
-      return;
-    }
-    if (var == 7) {
-      k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask,
-                                                         h->lut);
-      return;
-    }
-    if (var == 10) {
-      k_step_tiles_x<T, TN, M, true><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                               h->bmask, h->lut);
-      return;
-    }
-    if (var == 5 || var == 8) {
-      constexpr int MW = sizeof(T) == 4 ? 6 : 3;
-      if (h->n_items && var == 5)
-        k_step_tiles_w<T, TN, MW><<<(unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
-            pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
-      else if (h->n_items)
-        k_step_tiles_w<T, TN, MW, true><<<(unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
-            pre, post, h->flags, h->nbr27, bv, br, h->g, om, (const uint4*)h->items, h->n_items, h->lut);
-      return;
-    }
-    if (var == 3 || var == 4 || var == 1 || var == 2) {
-      if (var == 3)
-        k_step_tiles<T, TN, 3, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                             h->bmask, h->order, TH);
-      else if (var == 4)
-        k_step_tiles<T, TN, 4, MS><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                             h->bmask, h->order, TH);
-      else if (var == 1)
-        k_step_tiles<T, TN, 1, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                            h->bmask, h->order, TH);
-      else
-        k_step_tiles<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
-                                                            h->bmask, h->order, TH);
-      return;
-    }
+  if (wl) {
+    if (!h->n_items) return;
+    const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    const uint4* it = (const uint4*)h->items;
+    if (TH.on)  // the ghost exchange needs 48 registers (fp32)
+      k_step_tiles_w<T, TN, MW * 5 / 6, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
+          pre, post, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, TH);
+    else
+      k_step_tiles_w<T, TN, MW><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br,
+                                                                           h->g, om, it, h->n_items, lut);
+    return;
   }
-  k_step_tiles<T, TN, 2, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask,
-                                                      h->order, TH);
+  if (TH.on)
+    k_step_tiles_x<T, TN, MS, true, true><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om,
+                                                                     h->bmask, lut, TH);
+  else
+    k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
 }
 
 template <typename T, int TN>
@@ -413,37 +398,40 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   const T om = (T)h->d.omega;
+  const ulonglong2* lut = (const ulonglong2*)h->lut;
   constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;  // neighbour step: looser register cap (48)
-  if constexpr (TN == 512) {
-    // the warp work list where the AB step would use it (or when variant 5/8 is forced)
-    const bool wl = h->wlist_ok && (h->variant_set ? (h->variant == 5 || h->variant == 8) : h->auto_wlist);
-    if (wl) {
-      if (!h->n_items) return;
-      const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
-      const uint4* it = (const uint4*)h->items;
-      // 48 resident warps for both phases (40 registers; the neighbour step
-      // spills 8 B and still measured 0-1 % faster than 40 warps at 48
-      // registers, profiles/ab_aa_warp_list_r01.txt)
-      if (h->parity == 0)
-        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
-            F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
-      else
-        k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
-            F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, h->lut);
-      return;
-    }
+  // the warp work list where the AB step would use it
+  const bool wl = h->wlist_ok && (h->variant_set ? h->variant == 8 : h->auto_wlist);
+  if (wl) {
+    if (!h->n_items) return;
+    const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    const uint4* it = (const uint4*)h->items;
+    // 48 resident warps for both phases (40 registers; the neighbour step
+    // spills 8 B and still measured 0-1 % faster than 40 warps at 48
+    // registers, profiles/ab_aa_warp_list_r01.txt)
+    if (h->parity == 0)
+      k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
+          F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut);
+    else
+      k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
+          F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut);
+    return;
   }
   if (h->parity == 0)
-    k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order,
-                                                            h->lut);
+    k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
   else
-    k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, h->order,
-                                                           h->lut);
+    k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
 }
 
-// one step from `pre` into `post` (AB); AA updates `post` (== pre) in place
+// grid z-extent of a dense launch covering `zmode`'s planes (slab_z)
+unsigned zmode_planes(const Geo& g, int zmode) {
+  return zmode == 0 ? (unsigned)g.nz : (zmode == 1 ? (g.nz > 1 ? 2u : 1u) : (g.nz > 2 ? (unsigned)g.nz - 2u : 0u));
+}
+
+// one step from `pre` into `post` (AB); AA updates `post` (== pre) in place.
+// zmode (dense z-slabs): 0 every plane, 1 the two boundary planes, 2 the interior
 template <typename T>
-int launch_step(lbm_handle* h, const void* pre, void* post) {
+int launch_step(lbm_handle* h, const void* pre, void* post, int zmode = 0) {
   const Geo& g = h->g;
   const T om = (T)h->d.omega;
   Planes<T> P;
@@ -451,11 +439,14 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
     P.pre[i] = (const T*)pre + (size_t)i * g.ps;
     P.post[i] = (T*)post + (size_t)i * g.ps;
   }
-  // variants (LBM_STEP_VARIANT): 0 speculative + fix-up, 1 warp-uniform
-  // fast path else per-link select; 2 / 3 the same with a looser register cap
+  constexpr int D1 = sizeof(T) == 4 ? 12 : 6;
+#ifdef LBM_EXPERIMENTS
+  // variants (LBM_STEP_VARIANT): 1 warp-uniform fast path else per-link
+  // select; 2 / 3 the same with a looser register cap; 8 the 128-bit kernel
   const int var = h->variant;
-  constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
+  constexpr int D2 = sizeof(T) == 4 ? 10 : 5;
   constexpr int V4B = 3;  // 128-bit kernel: 3 x 128 threads per SM, up to 168 registers
+#endif
   const T* bv = (const T*)h->bcv;
   const T* br = (const T*)h->bcr;
   if (g.aa) {
@@ -463,12 +454,14 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
     if (!g.tiled) {
       Planes1<T> F;
       for (int i = 0; i < Q; ++i) F.f[i] = (T*)post + (size_t)i * g.ps;
-      dim3 grid((g.nxp + 127) / 128, g.ny, g.nz);
+      dim3 grid((g.nxp + 127) / 128, g.ny, zmode_planes(g, zmode));
+      if (grid.z == 0) return 0;
+      Halo<T> H = h->parity == 0 ? make_halo<T>(h, 0) : Halo<T>{};
+      H.zmode = zmode;
       if (h->parity == 0)
-        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om,
-                                                               make_halo<T>(h, 0));
+        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
       else
-        k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, Halo<T>{});
+        k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
     } else {
       if (h->n_tiles == 0) return 0;
       switch (g.tn) {
@@ -484,8 +477,13 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
   }
   if (!g.tiled) {
     const int bx = 128;
-    dim3 grid((g.nxp + bx - 1) / bx, g.ny, g.nz);
-    const Halo<T> H = make_halo<T>(h, 1 - h->parity);
+    dim3 grid((g.nxp + bx - 1) / bx, g.ny, zmode_planes(g, zmode));
+    if (grid.z == 0) return 0;
+    Halo<T> H = make_halo<T>(h, 1 - h->parity);
+    H.zmode = zmode;
+#ifdef LBM_EXPERIMENTS
+    // measured-slower alternatives, built only into the experiments library
+    // (python -m paper_2108_13241_b200.build --experiments; profiles/v4_r01.md)
     if (var == 1)
       k_step_dense<T, 1, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
     else if (var == 2)
@@ -503,19 +501,37 @@ int launch_step(lbm_handle* h, const void* pre, void* post) {
                                                        (float)om);
     }
     else
+#endif
       k_step_dense<T, 0, D1><<<grid, bx, 0, h->stream>>>(P, h->flags, h->ubits, bv, br, g, om, H);
   } else {
     if (h->n_tiles == 0) return 0;
     switch (g.tn) {
-      case 32: launch_tiles<T, 32>(h, (const T*)pre, (T*)post, var); break;
-      case 64: launch_tiles<T, 64>(h, (const T*)pre, (T*)post, var); break;
-      case 128: launch_tiles<T, 128>(h, (const T*)pre, (T*)post, var); break;
-      case 256: launch_tiles<T, 256>(h, (const T*)pre, (T*)post, var); break;
-      default: launch_tiles<T, 512>(h, (const T*)pre, (T*)post, var); break;
+      case 32: launch_tiles<T, 32>(h, (const T*)pre, (T*)post); break;
+      case 64: launch_tiles<T, 64>(h, (const T*)pre, (T*)post); break;
+      case 128: launch_tiles<T, 128>(h, (const T*)pre, (T*)post); break;
+      case 256: launch_tiles<T, 256>(h, (const T*)pre, (T*)post); break;
+      default: launch_tiles<T, 512>(h, (const T*)pre, (T*)post); break;
     }
   }
   h->launches += 1;
   return 0;
+}
+
+// one step of a connected z-slab: wait for the neighbours' previous step,
+// then (dense) the two boundary planes, the signal, and the interior -- the
+// neighbours' next step overlaps this slab's interior; tile slabs signal
+// after the whole step
+template <typename T>
+void slab_step(lbm_handle* h, const void* pre, void* post) {
+  halo_wait(h);
+  if (!h->g.tiled) {
+    launch_step<T>(h, pre, post, 1);
+    halo_signal(h);
+    launch_step<T>(h, pre, post, 2);
+  } else {
+    launch_step<T>(h, pre, post);
+    halo_signal(h);
+  }
 }
 
 // CUDA lazy module loading loads a kernel at its first launch, and loading
@@ -526,15 +542,13 @@ template <typename T, int TN>
 void preload_tiles(cudaFuncAttributes* a) {
   constexpr int BT = TN < 256 ? TN : 256;
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
-  if constexpr (TN == 512)
-    cudaFuncGetAttributes(a, k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true>);
-  else
-    cudaFuncGetAttributes(a, k_step_tiles<T, TN, 2, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true>);
+  cudaFuncGetAttributes(a, k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true>);
+  cudaFuncGetAttributes(a, k_step_tiles_w<T, TN, (sizeof(T) == 4 ? 6 : 3) * 5 / 6, true>);
 }
 
 template <typename T>
 void preload_halo_kernels(const lbm_handle* h) {
-  constexpr int D1 = sizeof(T) == 4 ? 12 : 6, D2 = sizeof(T) == 4 ? 10 : 5;
+  constexpr int D1 = sizeof(T) == 4 ? 12 : 6;
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, k_halo_wait);
   cudaFuncGetAttributes(&a, k_halo_signal);
@@ -544,9 +558,6 @@ void preload_halo_kernels(const lbm_handle* h) {
   } else if (!h->g.tiled) {
     cudaFuncGetAttributes(&a, k_halo_push<T>);
     cudaFuncGetAttributes(&a, k_step_dense<T, 0, D1>);
-    cudaFuncGetAttributes(&a, k_step_dense<T, 1, D1>);
-    cudaFuncGetAttributes(&a, k_step_dense<T, 0, D2>);
-    cudaFuncGetAttributes(&a, k_step_dense<T, 1, D2>);
   } else {
     cudaFuncGetAttributes(&a, k_tile_halo_push<T>);
     switch (h->g.tn) {
@@ -587,6 +598,15 @@ static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, 
   for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
   work(0);
   for (auto& x : th) x.join();
+}
+
+// Fresh caller arrays (np.empty) fault their pages in on the first write, 4 KB
+// at a time; asking for transparent huge pages first turns the readback's
+// fault-in into 2 MB faults (no-op where THP is off).
+static void advise_huge(void* p, size_t bytes) {
+  const uintptr_t a = ((uintptr_t)p + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+  const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((2u << 20) - 1);
+  if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
 }
 
 // Pipelined device -> host readback in z chunks: chunk k's kernel and D2H
@@ -815,10 +835,6 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
     h->variant_set = sv != nullptr;
     const char* ub = getenv("LBM_UBITS");
     h->use_ubits = !(ub && ub[0] == '0');
-    const char* to = getenv("LBM_TILE_ORDER");  // "row": launch tiles in rank order
-    // "morton" | "pencil[:B]" | "row" (rank order)
-    h->order_mode = !to ? 0 : to[0] == 'm' ? 1 : to[0] == 'p' ? 2 : to[0] == 'z' ? 3 : 0;
-    if (to && strchr(to, ':')) h->pencil = atoi(strchr(to, ':') + 1) > 0 ? atoi(strchr(to, ':') + 1) : 4;
     const char* gv = getenv("LBM_GRAPH");
     h->use_graph = !(gv && gv[0] == '0');
   }
@@ -842,8 +858,11 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
       const bool rows = bv && bv[0] == '0';
       const int want = d.dtype == LBM_F32 ? 3 : 2;  // log2(nodes per sector)
       int b[3] = {0, 0, 0}, left = want;
-      if (rows) {
+      if (rows) {  // x first, then y, z: a brick still fills one sector
         b[0] = want < g.lex ? want : g.lex;
+        left = want - b[0];
+        b[1] = left < g.ley ? left : g.ley;
+        b[2] = want - b[0] - b[1];
       } else {
         for (int a = 0; left > 0 && a < 3 * 4; ++a) {
           const int ax = a % 3, lim = ax == 0 ? g.lex : (ax == 1 ? g.ley : g.lez);
@@ -867,8 +886,8 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev1);
   if (e == cudaSuccess) e = cudaMalloc(&h->scratch, 4096 * sizeof(double));
   if (e == cudaSuccess) e = cudaMalloc(&h->uscratch, 4 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMalloc(&h->sync, 2 * sizeof(unsigned long long));
-  if (e == cudaSuccess) e = cudaMemset(h->sync, 0, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&h->sync, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(h->sync, 0, 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&h->herr, sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(h->herr, 0, sizeof(int));
   if (e != cudaSuccess) {
@@ -1055,26 +1074,6 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         k_tile_nbr<<<(unsigned)((T * 27 + 255) / 256), 256, 0, h->stream>>>(h->nbr27, h->tiles, h->rank, g, T);
         CKL();
       }
-      if (T > 0 && h->order_mode) {
-        unsigned long long *k0 = nullptr, *k1 = nullptr;
-        int* v0 = nullptr;
-        void* st = nullptr;
-        size_t sb = 0;
-        if ((rc = dev_alloc(h, &k0, T * 8)) || (rc = dev_alloc(h, &k1, T * 8)) || (rc = dev_alloc(h, &v0, T * 4)) ||
-            (rc = dev_alloc(h, &h->order, T * 4)))
-          goto done;
-        k_tile_order_key<<<(unsigned)((T + 255) / 256), 256, 0, h->stream>>>(k0, v0, h->tiles, T, h->order_mode,
-                                                                             h->pencil, g);
-        CKL();
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, k0, k1, v0, h->order, (int)T, 0, 63, h->stream));
-        if ((rc = dev_alloc(h, (char**)&st, sb))) goto done;
-        CK(cub::DeviceRadixSort::SortPairs(st, sb, k0, k1, v0, h->order, (int)T, 0, 63, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
-        dev_free(k0);
-        dev_free(k1);
-        dev_free(v0);
-        dev_free(st);
-      }
       h->n_slots = T * g.tn;
       g.ps = h->n_slots;  // AoSoA: 19 * ps elements = T tiles x 19 blocks
       h->nflags = h->n_slots;
@@ -1113,13 +1112,8 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           h->wlist_ok = per <= 8;
           std::vector<uint32_t> it;
           it.reserve((size_t)(live / per + T) * 4);
-          std::vector<int> ho;  // LBM_TILE_ORDER also orders the work list
-          if (h->order && T > 0) {
-            ho.resize(T);
-            CK(scopy(h, ho.data(), h->order, T * 4, cudaMemcpyDeviceToHost));
-          }
           for (long long k2 = 0; h->wlist_ok && k2 < T; ++k2) {
-            const long long t = ho.empty() ? k2 : ho[k2];
+            const long long t = k2;
             uint32_t rec[4] = {(uint32_t)t, 0u, 0u, 0u};
             int k = 0;
             for (int q = 0; q < 4; ++q) {
@@ -1153,29 +1147,37 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         h->live_frac = live_frac;
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag
         // words; the work list when it is used
-        h->meta_bytes = T * (27 * 4 + 32 + (h->order ? 4 : 0)) + (live - uni) * bn * 4 +
+        h->meta_bytes = T * (27 * 4 + 32) + (live - uni) * bn * 4 +
                         (h->auto_wlist ? (long long)h->n_items * 16 : 0);
       }
       h->sm.rank = h->rank;
       {
-        // per-slot neighbour table for the tile kernels (TileUpLUT)
-        std::vector<unsigned long long> lt(g.tn);
+        // per-slot neighbour table for the tile kernels (TileUpLUT): in-tile
+        // slot deltas per axis (the slot order is separable over x / y / z)
+        auto P = [](int l) { return l; };
+        std::vector<unsigned long long> lt(2 * (size_t)g.tn);
         for (int l = 0; l < g.tn; ++l) {
           int lx, ly, lz;
           brick_inv(g, l, lx, ly, lz);
           const int e[3] = {g.ex, g.ey, g.ez}, c[3] = {lx, ly, lz};
-          unsigned long long w = 0;
+          int mag[6];
+          unsigned cross = 0;
           for (int a = 0; a < 3; ++a) {
             auto br = [&](int v) { return a == 0 ? brick_x(g, v) : (a == 1 ? brick_y(g, v) : brick_z(g, v)); };
-            const int own = br(c[a]);
+            const int own = P(br(c[a]));
             const bool cm = c[a] == 0, cp = c[a] == e[a] - 1;
-            const int mm = br(cm ? e[a] - 1 : c[a] - 1) - own, mp = br(cp ? 0 : c[a] + 1) - own;
-            w |= (unsigned long long)(mm < 0 ? -mm : mm) << (18 * a);
-            w |= (unsigned long long)(mp < 0 ? -mp : mp) << (18 * a + 9);
-            w |= (unsigned long long)cm << (54 + 2 * a);
-            w |= (unsigned long long)cp << (55 + 2 * a);
+            const int mm = P(br(cm ? e[a] - 1 : c[a] - 1)) - own, mp = P(br(cp ? 0 : c[a] + 1)) - own;
+            mag[2 * a] = mm < 0 ? -mm : mm;
+            mag[2 * a + 1] = mp < 0 ? -mp : mp;
+            cross |= (cm ? 1u : 0u) << (2 * a);
+            cross |= (cp ? 1u : 0u) << (2 * a + 1);
           }
-          lt[l] = w;
+          unsigned long long x = 0, y = 0;
+          for (int k = 0; k < 4; ++k) x |= (unsigned long long)mag[k] << (14 * k);
+          x |= (unsigned long long)cross << 56;
+          y = (unsigned long long)mag[4] | (unsigned long long)mag[5] << 14 | (unsigned long long)P(l) << 32;
+          lt[2 * l] = x;
+          lt[2 * l + 1] = y;
         }
         if ((rc = dev_alloc(h, &h->lut, lt.size() * 8))) goto done;
         CK(scopy(h, h->lut, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice));
@@ -1206,7 +1208,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     }
     pt.mark("geometry done");
     // PDF buffers
-    const size_t fbytes = (size_t)Q * (size_t)(g.ps > 0 ? g.ps : 64) * h->esize;
+    const size_t fbytes = (size_t)(buf_elems(h) > 0 ? buf_elems(h) : 64) * h->esize;
     if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes))) goto done;
     if (!g.aa && (rc = dev_alloc(h, (char**)&h->f[1], fbytes))) goto done;  // AA: one buffer
     CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->stream));
@@ -1231,8 +1233,8 @@ done:
     dev_free(cub_tmp);
     // recompute resident bytes (temporaries released)
     if (h->geometry) {
-      long long b = (h->g.aa ? 1LL : 2LL) * Q * (h->g.ps > 0 ? h->g.ps : 64) * h->esize + h->nflags * 4;
-      if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * (30 + 8 + (h->order ? 1 : 0)) * 4;
+      long long b = (h->g.aa ? 1LL : 2LL) * (buf_elems(h) > 0 ? buf_elems(h) : 64) * h->esize + h->nflags * 4;
+      if (h->g.tiled) b += h->ntiles_grid * 4 + h->n_tiles * (30 + 8) * 4;
       if (h->gh[0]) b += 2LL * 10 * h->g.nx * h->g.ny * h->esize;
       h->device_bytes = b;
     }
@@ -1262,7 +1264,7 @@ int lbm_init_equilibrium(lbm_t* h, const double* rho, const double* ux, const do
     if (e != cudaSuccess) rc = fail(LBM_ECUDA, "init upload: %s", cudaGetErrorString(e));
   }
   if (!rc) {
-    const size_t fbytes = (size_t)Q * g.ps * h->esize;
+    const size_t fbytes = (size_t)buf_elems(h) * h->esize;
     cudaMemsetAsync(h->f[0], 0, fbytes, h->stream);
     if (h->f[1]) cudaMemsetAsync(h->f[1], 0, fbytes, h->stream);
     h->parity = 0;
@@ -1317,22 +1319,27 @@ int lbm_step_async(lbm_t* h, int64_t n) {
   CK(cudaEventRecord(h->ev0, h->stream));
   // launch-bound small domains: replay a captured CUDA graph of kGraphSteps
   // steps (an even count, so it starts and ends on the same parity)
-  if (!halo && h->use_graph && n >= kGraphSteps) {
+  // z-slabs capture their wait / boundary / signal / interior sequence too
+  // (the epochs live on the device)
+  if (h->use_graph && n >= kGraphSteps) {
     cudaGraphExec_t& ge = h->graph[h->parity];
+    const long long l0 = h->launches;
     if (!ge) {
       cudaGraph_t gr = nullptr;
       const int p0 = h->parity;
-      const long long l0 = h->launches;
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       for (int k = 0; k < kGraphSteps; ++k) {
-        if (h->esize == 4)
-          launch_step<float>(h, pre_buf(h), h->g.aa ? h->f[0] : h->f[1 - h->parity]);
-        else
-          launch_step<double>(h, pre_buf(h), h->g.aa ? h->f[0] : h->f[1 - h->parity]);
+        void* post = h->g.aa ? h->f[0] : h->f[1 - h->parity];
+        if (h->esize == 4) {
+          if (halo) slab_step<float>(h, pre_buf(h), post); else launch_step<float>(h, pre_buf(h), post);
+        } else {
+          if (halo) slab_step<double>(h, pre_buf(h), post); else launch_step<double>(h, pre_buf(h), post);
+        }
         h->parity ^= 1;
       }
       CK(cudaStreamEndCapture(h->stream, &gr));
       h->parity = p0;
+      h->graph_launches = h->launches - l0;
       h->launches = l0;
       cudaError_t e = cudaGraphInstantiate(&ge, gr, 0);
       cudaGraphDestroy(gr);
@@ -1340,7 +1347,7 @@ int lbm_step_async(lbm_t* h, int64_t n) {
     }
     while (n >= kGraphSteps) {
       CK(cudaGraphLaunch(ge, h->stream));
-      h->launches += kGraphSteps;
+      h->launches += h->graph_launches;
       n -= kGraphSteps;
       h->step_count += kGraphSteps;
       h->visited_total += kGraphSteps * visits_per_step(h);
@@ -1349,12 +1356,12 @@ int lbm_step_async(lbm_t* h, int64_t n) {
   for (int64_t k = 0; k < n; ++k) {
     const void* pre = pre_buf(h);
     void* post = h->g.aa ? h->f[0] : h->f[1 - h->parity];
-    if (halo) halo_wait(h);   // neighbours pushed my ghosts and finished reading theirs
-    if (h->esize == 4)
-      launch_step<float>(h, pre, post);
-    else
-      launch_step<double>(h, pre, post);
-    if (halo) halo_signal(h);
+    // slabs: neighbours pushed my ghosts and finished reading theirs
+    if (h->esize == 4) {
+      if (halo) slab_step<float>(h, pre, post); else launch_step<float>(h, pre, post);
+    } else {
+      if (halo) slab_step<double>(h, pre, post); else launch_step<double>(h, pre, post);
+    }
     h->parity ^= 1;
   }
   CKL();
@@ -1428,6 +1435,7 @@ int lbm_get_macroscopic(lbm_t* h, double* rho, double* ux, double* uy, double* u
       k_macro<double><<<grid, 128, 0, h->stream>>>((const double*)pre_buf(h), h->flags, h->sm, g, z0, f[0], f[1],
                                                    f[2], f[3]);
   };
+  for (int j = 0; j < nf; ++j) advise_huge(outs[which[j]], (size_t)h->n_nodes * 8);
   auto consume = [&](int, int z0, int nzc, const char* pin) {
     const long long C = (long long)nzc * pn;
     std::vector<std::pair<char*, const char*>> ds;
@@ -1560,6 +1568,7 @@ static int pdf_io(lbm_t* h, int which, void* host, bool get) {
   char* hb = (char*)host;
   if (get) {
     cudaFree(d);
+    advise_huge(host, (size_t)Q * N * es);
     // pipelined: chunk = (19, nzc * pn) in the storage type
     auto launch = [&](int, int z0, int nzc, char* dev) {
       const dim3 grid((g.nx + 127) / 128, g.ny, nzc);
@@ -1631,7 +1640,7 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   if (h->g.aa && which != 0) return fail(LBM_EINVAL, "the AA scheme keeps one buffer: there is no post buffer");
   DeviceGuard dg(h->d.device);
-  const size_t bytes = (size_t)Q * h->g.ps * h->esize;
+  const size_t bytes = (size_t)buf_elems(h) * h->esize;
   if (h->g.aa) {
     // decoded pre buffer in the native slot order, staged on the device
     void* d = nullptr;
@@ -1744,7 +1753,7 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->scheme = h->d.scheme;
   // z-slab tile handles (ghost planes) run the CTA-per-tile exchange kernel
   s->tile_work_list = h->gh[0] == nullptr && h->wlist_ok &&
-      ((h->auto_wlist && !h->variant_set) || (h->g.tiled && (h->variant == 5 || h->variant == 8))) ? 1 : 0;
+      ((h->auto_wlist && !h->variant_set) || (h->g.tiled && h->variant == 8)) ? 1 : 0;
   return 0;
 }
 
@@ -1851,6 +1860,7 @@ int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
     if ((rc = open_peer(h, b, h->hi))) return rc;
   }
   if (h->esize == 4) preload_halo_kernels<float>(h); else preload_halo_kernels<double>(h);
+  drop_graphs(h);  // captured step sequences change with the neighbours
   h->halo_dirty = true;
   return 0;
 }

@@ -25,12 +25,22 @@ template <typename T>
 struct Halo {
   T* lo[5];  // lower neighbour's upper ghost plane, directions kZm
   T* hi[5];  // upper neighbour's lower ghost plane, directions kZp
+  int zmode; // planes this launch covers: 0 all, 1 the two boundary planes, 2 the interior
 };
 
-__global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int need_hi,
-                            unsigned long long target, int* err) {
+// z of this block under a Halo's zmode (boundary planes first on z-slabs,
+// so the neighbours may start their next step while the interior runs)
+__device__ __forceinline__ int slab_z(int bz, int zmode, int nz) {
+  return zmode == 0 ? bz : (zmode == 1 ? (bz ? nz - 1 : 0) : bz + 1);
+}
+
+// Ordering words (device memory): sync[0] written by the lower neighbour,
+// sync[1] by the upper one, sync[2] this slab's own epoch.  The epoch lives
+// on the device, so wait / step / signal sequences replay from a CUDA graph.
+__global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int need_hi, int* err) {
   const long long t0 = clock64();
   const volatile unsigned long long* vs = sync;
+  const unsigned long long target = vs[2];
   while ((need_lo && vs[0] < target) || (need_hi && vs[1] < target)) {
     __nanosleep(200);
     if (clock64() - t0 > 60LL * 2000000000LL) {  // ~1 min at 2 GHz: a neighbour is gone
@@ -42,7 +52,9 @@ __global__ void k_halo_wait(const unsigned long long* sync, int need_lo, int nee
 }
 
 __global__ void k_halo_signal(unsigned long long* lo_slot, unsigned long long* hi_slot,
-                              unsigned long long value) {
+                              unsigned long long* own) {
+  const unsigned long long value = *own + 1;
+  *own = value;
   __threadfence_system();
   if (lo_slot) *(volatile unsigned long long*)lo_slot = value;
   if (hi_slot) *(volatile unsigned long long*)hi_slot = value;
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
                                                    const T* __restrict__ bcr, Geo g, T om,
                                                    const Halo<T> H) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int y = blockIdx.y, z = slab_z(blockIdx.z, H.zmode, g.nz);
   if (x >= g.nxp) return;  // whole warps (nxp % 32 == 0)
   // 32-bit unsigned slot arithmetic (slabs up to 2^32 slots; negative
   // offsets wrap modulo 2^32 and land on the right slot)
@@ -218,6 +230,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense(const Planes<T> P, con
   }
 }
 
+#ifdef LBM_EXPERIMENTS
 // Dense AB step with 128-bit accesses: four consecutive x-nodes per thread,
 // 19 LDG.128 + 19 STG.128 per quad.  Directions with c_x = 0 load the
 // upstream quad directly; c_x = +-1 load the aligned quad of the upstream row
@@ -303,6 +316,7 @@ k_step_dense_v4(const Planes<float> P, const uint32_t* __restrict__ flags, const
 #pragma unroll
   for (int i = 0; i < Q; ++i) *reinterpret_cast<float4*>(P.post[i] + s) = v[i];
 }
+#endif  // LBM_EXPERIMENTS
 
 // A-A in place (LBM_SCHEME_AA): one buffer F, two alternating kernels, each
 // node reading and writing only locations no other node touches in the same
@@ -361,7 +375,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
                                                       const T* __restrict__ bcv, const T* __restrict__ bcr,
                                                       Geo g, T om, const Halo<T> H) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y, z = blockIdx.z;
+  const int y = blockIdx.y, z = slab_z(blockIdx.z, H.zmode, g.nz);
   if (x >= g.nxp) return;
   const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
   const unsigned s = fi + (unsigned)g.plane;

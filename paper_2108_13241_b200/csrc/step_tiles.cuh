@@ -1,39 +1,48 @@
-// Sparse tile step kernels (AoSoA tiles, nbr27, live bricks): AB variants,
-// z-slab ghost exchange, warp work list, shared-memory staging, A-A.
+// Sparse tile step kernels over brick records (AB: warp work list and
+// CTA per tile, with the z-slab ghost exchange; A-A in place).
 // Part of liblbm19 (included once, in order, by lbm19.cu).
 #pragma once
 
-// Sparse tiles, AoSoA storage f[tile][i][TN]: one CTA per kept tile.  All
-// addresses are 32-bit element offsets from the CTA's own tile block; the
-// upstream slot of direction i is separable per axis (tile code
-// (dx+1) + 3(dy+1) + 9(dz+1), relative tile offset from shared memory, and
-// in-tile offset lx' + ex ly' + ex ey lz'), and every own-tile access
-// (bounce-back, stores) has a compile-time offset i*TN.
+// Storage (tile layouts): AoSoA f[tile][direction][in-tile slot], each
+// (tile, direction) block contiguous (TN elements: 2 KB for 512 fp32 nodes),
+// in-tile slots in sector-brick order (layout.cuh).  Element of (direction
+// i, in-tile slot l) of tile t: t * (Q * TN) + i * TN + l.
+//
+// Measured alternative (round 2, profiles/ab_brick_records_r02.txt): 640-B
+// brick records (19 direction sectors of one brick + pad, so a 128-B line
+// never mixes live and dead bricks) cut the DRAM reads of the porous
+// configs' partly live lines, but a warp's four bricks then touch four lines
+// per load instead of one: +5 % at phi = 0.1, -9 to -26 % at phi >= 0.2 and
+// on the vascular forest.  The per-direction blocks stay.
 
-// Live-brick work list of one tile (MODE 2): threads cover only the tile's
-// live bricks (sector-sized bricks holding >= 1 non-solid node, a 128-bit
-// mask per tile), so a sparse tile costs lanes in proportion to its live
-// sectors, not its TN slots.  Words 4-7 of the mask mark uniform bricks
+template <typename T>
+struct Rec {
+  static constexpr int BN = 32 / (int)sizeof(T);  // nodes per brick (one sector)
+};
+
+// Live-brick enumeration of one tile for the CTA-per-tile kernels: threads
+// cover only the tile's live bricks (sector-sized bricks holding >= 1
+// non-solid node, a 128-bit mask per tile), so a sparse tile costs lanes in
+// proportion to its live sectors.  Words 4-7 of the mask mark uniform bricks
 // (all FLUID / wall with full masks) whose flag words the step skips.
 struct TileBricks {
   uint32_t m[4], u[4];
   int pre_cnt[4];
   int work, lbn, bn;
   bool dense_tile;
-  __device__ __forceinline__ TileBricks(const uint32_t* __restrict__ bmask, long long t, const Geo& g, int tn,
-                                        bool compact) {
+  __device__ __forceinline__ TileBricks(const uint32_t* __restrict__ bmask, long long t, const Geo& g, int tn) {
     lbn = g.lbx + g.lby + g.lbz;
     bn = 1 << lbn;
     int acc = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       u[q] = __ldg(bmask + 8LL * t + 4 + q);
-      m[q] = compact ? __ldg(bmask + 8LL * t + q) : 0u;
+      m[q] = __ldg(bmask + 8LL * t + q);
       pre_cnt[q] = acc;
       acc += __popc(m[q]);
     }
-    work = compact ? ((acc << lbn) + 31) & ~31 : tn;  // whole warps; lanes past acc*bn idle
-    dense_tile = !compact || acc == (tn >> lbn);       // every brick live: identity mapping
+    work = ((acc << lbn) + 31) & ~31;   // whole warps; lanes past acc*bn idle
+    dense_tile = acc == (tn >> lbn);    // every brick live: identity mapping
   }
   // in-tile slot of work item k; `in` false for idle lanes past the last live brick
   __device__ __forceinline__ int slot(int k, bool& in) const {
@@ -61,75 +70,52 @@ struct TileBricks {
   }
 };
 
-// offset (from the own tile's block, excluding the direction plane) of the
-// node x - c_i: neighbour tile from the shared relative-offset table,
-// in-tile position from the separable brick order
-struct TileUp {
-  int cxm, lxm, cxp, lxp, cym, lym, cyp, lyp, czm, lzm, czp, lzp, lx0, ly0, lz0;
-  __device__ __forceinline__ TileUp(const Geo& g, int l) {
-    int lx, ly, lz;
-    brick_inv(g, l, lx, ly, lz);
-    // c = +1 pulls from l - 1, c = -1 from l + 1: (tile-code delta, in-tile offset)
-    cxm = lx == 0 ? -1 : 0, lxm = brick_x(g, lx == 0 ? g.ex - 1 : lx - 1);
-    cxp = lx == g.ex - 1 ? 1 : 0, lxp = brick_x(g, lx == g.ex - 1 ? 0 : lx + 1);
-    cym = ly == 0 ? -3 : 0, lym = brick_y(g, ly == 0 ? g.ey - 1 : ly - 1);
-    cyp = ly == g.ey - 1 ? 3 : 0, lyp = brick_y(g, ly == g.ey - 1 ? 0 : ly + 1);
-    czm = lz == 0 ? -9 : 0, lzm = brick_z(g, lz == 0 ? g.ez - 1 : lz - 1);
-    czp = lz == g.ez - 1 ? 9 : 0, lzp = brick_z(g, lz == g.ez - 1 ? 0 : lz + 1);
-    lx0 = brick_x(g, lx), ly0 = brick_y(g, ly), lz0 = brick_z(g, lz);
-  }
-  __device__ __forceinline__ int code(int i) const {
-    return 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) + (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
-           (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
-  }
-  __device__ __forceinline__ int loc(int i) const {
-    return (cx(i) == 1 ? lxm : (cx(i) == -1 ? lxp : lx0)) + (cy(i) == 1 ? lym : (cy(i) == -1 ? lyp : ly0)) +
-           (cz(i) == 1 ? lzm : (cz(i) == -1 ? lzp : lz0));
-  }
-  __device__ __forceinline__ int at(const int* srel, int i) const { return srel[code(i)] + loc(i); }
-};
-
-// The same offsets from a per-slot table (one u64 per in-tile slot, built
-// on the host for the handle's tile shape, L1-resident): bits 0-53 hold the
-// six in-tile brick-order deltas' magnitudes (9 bits each: x-, x+, y-, y+,
-// z-, z+), bits 54-59 whether the neighbour lies across the tile face (the
-// delta is then positive -- a wrap inside the neighbour tile -- else
-// negative for "-" and positive for "+").
+// Per in-tile slot neighbour table (built on the host for the handle's tile
+// shape, 16 B per slot, L1-resident).  x: bits 0-55 the magnitudes of the
+// in-tile slot deltas (14 bits each) to the x-, x+, y-, y+ neighbours, bits
+// 56-61 whether each of the six neighbours lies across the tile face (the
+// delta is then a wrap inside the neighbour tile: positive for "-", negative
+// for "+"); y: bits 0-27 the z-, z+ magnitudes, bits 32-47 the slot itself.
 struct TileUpLUT {
-  int l, dxm, dxp, dym, dyp, dzm, dzp, cxm, cxp, cym, cyp, czm, czp;
-  __device__ __forceinline__ TileUpLUT(const unsigned long long* __restrict__ lut, int slot) : l(slot) {
-    const unsigned long long e = __ldg(lut + slot);
-    const int mag[6] = {(int)(e & 511), (int)(e >> 9 & 511), (int)(e >> 18 & 511), (int)(e >> 27 & 511),
-                        (int)(e >> 36 & 511), (int)(e >> 45 & 511)};
-    const unsigned cr = (unsigned)(e >> 54) & 63u;
-    dxm = (cr & 1) ? mag[0] : -mag[0];
-    dxp = mag[1] * ((cr & 2) ? -1 : 1);
-    dym = (cr & 4) ? mag[2] : -mag[2];
-    dyp = mag[3] * ((cr & 8) ? -1 : 1);
-    dzm = (cr & 16) ? mag[4] : -mag[4];
-    dzp = mag[5] * ((cr & 32) ? -1 : 1);
+  int p, dxm, dxp, dym, dyp, dzm, dzp, cxm, cxp, cym, cyp, czm, czp;
+  __device__ __forceinline__ TileUpLUT(const ulonglong2* __restrict__ lut, int slot) {
+    const ulonglong2 e = __ldg(lut + slot);
+    const unsigned cr = (unsigned)(e.x >> 56) & 63u;
+    const int m0 = (int)(e.x & 16383u), m1 = (int)(e.x >> 14 & 16383u), m2 = (int)(e.x >> 28 & 16383u),
+              m3 = (int)(e.x >> 42 & 16383u), m4 = (int)(e.y & 16383u), m5 = (int)(e.y >> 14 & 16383u);
+    p = (int)(e.y >> 32 & 65535u);
+    dxm = (cr & 1) ? m0 : -m0;
+    dxp = (cr & 2) ? -m1 : m1;
+    dym = (cr & 4) ? m2 : -m2;
+    dyp = (cr & 8) ? -m3 : m3;
+    dzm = (cr & 16) ? m4 : -m4;
+    dzp = (cr & 32) ? -m5 : m5;
     cxm = (cr & 1) ? -1 : 0, cxp = (cr & 2) ? 1 : 0;
     cym = (cr & 4) ? -3 : 0, cyp = (cr & 8) ? 3 : 0;
     czm = (cr & 16) ? -9 : 0, czp = (cr & 32) ? 9 : 0;
   }
+  // tile code (dx+1) + 3(dy+1) + 9(dz+1) of the node x - c_i
   __device__ __forceinline__ int code(int i) const {
     return 13 + (cx(i) == 1 ? cxm : (cx(i) == -1 ? cxp : 0)) + (cy(i) == 1 ? cym : (cy(i) == -1 ? cyp : 0)) +
            (cz(i) == 1 ? czm : (cz(i) == -1 ? czp : 0));
   }
+  // in-tile slot of the node x - c_i (in the tile given by code(i))
   __device__ __forceinline__ int loc(int i) const {
-    return l + (cx(i) == 1 ? dxm : (cx(i) == -1 ? dxp : 0)) + (cy(i) == 1 ? dym : (cy(i) == -1 ? dyp : 0)) +
+    return p + (cx(i) == 1 ? dxm : (cx(i) == -1 ? dxp : 0)) + (cy(i) == 1 ? dym : (cy(i) == -1 ? dyp : 0)) +
            (cz(i) == 1 ? dzm : (cz(i) == -1 ? dzp : 0));
   }
 };
 
-// stage the 27 neighbour ranks as relative element offsets (absent: 0, i.e.
-// the own tile -- such links are masked)
-template <int TN>
-__device__ __forceinline__ void stage_nbr(int* srel, const int* __restrict__ nbr27, int t) {
-  if (threadIdx.x < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + threadIdx.x);
-    srel[threadIdx.x] = v < 0 ? 0 : (v - t) * (Q * TN);
+// the 27 neighbour ranks of tile t as element offsets relative to the tile,
+// one per lane (lanes 0-26; absent: 0, i.e. the own tile -- such links are masked)
+template <typename T, int TN>
+__device__ __forceinline__ int nbr_rel(const int* __restrict__ nbr27, int t, int lane) {
+  int srel = 0;
+  if (lane < 27) {
+    const int v = __ldg(nbr27 + 27LL * t + lane);
+    srel = v < 0 ? 0 : (v - t) * (Q * TN);
   }
+  return srel;
 }
 
 // z-slab halo for tile layouts: ghost planes (5 populations x ny x nx, row
@@ -207,96 +193,21 @@ __global__ void k_tile_halo_push(const T* __restrict__ pre, SlotMap sm, Geo g, T
   __threadfence_system();
 }
 
-// MODE 0: speculative pull + fix-up over all TN slots; MODE 1: select per
-// link (no masked link fetches a byte); MODE 2: MODE 0 over live bricks only;
-// MODE 3: MODE 1 over live bricks; MODE 4: live bricks, warps whose live
-// nodes all have full masks pull unconditionally, the others select per link.
-template <typename T, int TN, int MODE, int MINB, bool CUT = false>
-__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
-k_step_tiles(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-             const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-             const uint32_t* __restrict__ bmask, const int* __restrict__ order, const TileHalo<T> TH) {
-  constexpr int BT = TN < 256 ? TN : 256;
-  __shared__ int srel[27];
-  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
-  stage_nbr<TN>(srel, nbr27, t);
-  // z-slab cut: tiles on the first / last tile plane exchange their boundary
-  // nodes' c_z populations through ghost planes (uniform per CTA)
-  int tz0 = 0, tx0 = 0, ty0 = 0;
-  bool cut = false;
-  if (CUT) {
-    tx0 = __ldg(TH.tiles + 3 * t) * g.ex;
-    ty0 = __ldg(TH.tiles + 3 * t + 1) * g.ey;
-    tz0 = __ldg(TH.tiles + 3 * t + 2) * g.ez;
-    cut = tz0 == 0 || tz0 + g.ez >= g.nz;
-  }
-  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-  T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  constexpr bool kCompact = MODE >= 2;
-  constexpr bool kSelect = MODE == 1 || MODE == 3;
-  const TileBricks tw(bmask, t, g, TN, kCompact);
-  __syncthreads();
-#pragma unroll 1
-  for (int k = threadIdx.x; k < tw.work; k += BT) {
-    bool in;
-    const int l = tw.slot(k, in);
-    const uint32_t w = tw.flag(flags, t, TN, l, in);
-    const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    const uint32_t miss = ~w & kMaskBits;
-    const bool fast = MODE == 4 ? __all_sync(0xffffffffu, !live || miss == 0u) : !kSelect;
-    if (!live) {
-      if (zfill && in) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
-      }
-      continue;
-    }
-    const TileUp up(g, l);
-    T f[Q];
-    f[0] = __ldg(tb + l);
-    if (fast) {
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = __ldg(tb + i * TN + up.at(srel, i));
-      if (miss) {
-#pragma unroll
-        for (int i = 1; i < Q; ++i)
-          if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
-      }
-    } else {
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? opp(i) * TN + l : i * TN + up.at(srel, i)));
-    }
-    int x = 0, y = 0, z = -1;
-    if (CUT && cut) {
-      brick_inv(g, l, x, y, z);
-      x += tx0;
-      y += ty0;
-      z += tz0;
-      tile_ghost_gather<T>(f, miss, TH, g, x, y, z);
-    }
-    bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
-    if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
-  }
-}
-
-// MODE 7: the live-brick CTA-per-tile kernel without the shared-memory
-// neighbour table and its block barrier: every warp keeps the 27 relative
-// tile offsets in lanes 0-26 and fetches them with shuffles (all lanes take
-// part, so the offsets are formed before dead lanes leave the iteration).
+// One CTA per kept tile, threads over the tile's live bricks.  Every warp
+// keeps the 27 relative tile offsets in lanes 0-26 and fetches them with
+// shuffles (all lanes take part, so the offsets are formed before dead lanes
+// leave the iteration).  SEL: exact per-link select (a masked link never
+// fetches the -- solid -- upstream slot); else speculative pull + bounce-back
+// fix-up.  CUT: z-slab, tiles on the first / last tile plane exchange their
+// boundary nodes' c_z populations through ghost planes (uniform per CTA).
 template <typename T, int TN, int MINB, bool SEL = false, bool CUT = false>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask, const unsigned long long* __restrict__ lut,
+               const uint32_t* __restrict__ bmask, const ulonglong2* __restrict__ lut,
                const TileHalo<T> TH = TileHalo<T>{}) {
   constexpr int BT = TN < 256 ? TN : 256;
   const int t = blockIdx.x;
-  // z-slab cut (CUT): tiles on the first / last tile plane exchange their
-  // boundary nodes' c_z populations through ghost planes (uniform per CTA)
   int tz0 = 0, tx0 = 0, ty0 = 0;
   bool cut = false;
   if (CUT) {
@@ -306,14 +217,10 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
     cut = tz0 == 0 || tz0 + g.ez >= g.nz;
   }
   const int lane = threadIdx.x & 31;
-  int srel = 0;
-  if (lane < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + lane);
-    srel = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
+  const int srel = nbr_rel<T, TN>(nbr27, t, lane);
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
   T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, true);
+  const TileBricks tw(bmask, t, g, TN);
 #pragma unroll 1
   for (int k = threadIdx.x - lane; k < tw.work; k += BT) {  // whole warps
     const int kk = k + lane;
@@ -329,20 +236,20 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
     if (!live) {
       if (zfill && in) {
 #pragma unroll
-        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+        for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = (T)0;
       }
       continue;
     }
     const uint32_t miss = ~w & kMaskBits;
     T f[Q];
-    f[0] = __ldg(tb + l);
+    f[0] = __ldg(tb + up.p);
 #pragma unroll
-    for (int i = 1; i < Q; ++i)  // SEL: masked links never fetch the (solid) upstream slot
-      f[i] = __ldg(tb + ((SEL && ((miss >> (opp(i) - 1)) & 1u)) ? opp(i) * TN + l : i * TN + off[i]));
+    for (int i = 1; i < Q; ++i)
+      f[i] = __ldg(tb + ((SEL && ((miss >> (opp(i) - 1)) & 1u)) ? up.p + opp(i) * TN : off[i] + i * TN));
     if (!SEL && miss) {
 #pragma unroll
       for (int i = 1; i < Q; ++i)
-        if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + up.p + opp(i) * TN);
     }
     int x = 0, y = 0, z = -1;
     if (CUT && cut) {
@@ -354,87 +261,8 @@ k_step_tiles_x(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
     }
     bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+    for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = f[i];
     if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
-  }
-}
-
-// Shared-memory tile staging (MODE 6): pass 1 stages the tile's live bricks
-// (each thread its own nodes' 19 values, coalesced) in shared memory; after
-// one barrier, pass 2 gathers in-tile upstream values from shared memory and
-// only face links from global memory (the neighbour tiles, mostly L2 hits).
-// This cuts the L1 -> L2 sector traffic of the brick-shifted gathers, which
-// is 2-3x the DRAM traffic in the direct kernel.
-template <typename T, int TN, int MINB>
-__global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
-k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-               const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint32_t* __restrict__ bmask) {
-  constexpr int BT = TN < 256 ? TN : 256;
-  constexpr int IT = TN / BT;  // passes per thread
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* sf = reinterpret_cast<T*>(smem_raw);  // [Q][TN], same order as the tile block
-  __shared__ int srel[27];
-  const int t = blockIdx.x;
-  stage_nbr<TN>(srel, nbr27, t);
-  const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-  T* __restrict__ tp = post + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, true);
-  int ls[IT];
-  uint32_t ws[IT];
-  bool ins[IT];
-#pragma unroll
-  for (int p = 0; p < IT; ++p) {
-    const int k = threadIdx.x + p * BT;
-    ins[p] = false;
-    ls[p] = 0;
-    ws[p] = 0u;
-    if (k < tw.work) {
-      bool in;
-      const int l = tw.slot(k, in);
-      ls[p] = l;
-      ins[p] = in;
-      ws[p] = tw.flag(flags, t, TN, l, in);
-      if (in) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) sf[i * TN + l] = __ldg(tb + i * TN + l);
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int p = 0; p < IT; ++p) {
-    const int k = threadIdx.x + p * BT;
-    if (k >= tw.work) break;  // whole warps (work is a multiple of 32)
-    const int l = ls[p];
-    const uint32_t w = ws[p];
-    const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    if (!live) {
-      if (zfill && ins[p]) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
-      }
-      continue;
-    }
-    const uint32_t miss = ~w & kMaskBits;
-    const TileUp up(g, l);
-    T f[Q];
-    f[0] = sf[l];
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-      const int c = up.code(i);
-      // in-tile upstream (code 13) from shared memory, face links from global
-      f[i] = c == 13 ? sf[i * TN + up.loc(i)] : __ldg(tb + srel[c] + i * TN + up.loc(i));
-    }
-    if (miss) {
-#pragma unroll
-      for (int i = 1; i < Q; ++i)
-        if ((miss >> (opp(i) - 1)) & 1u) f[i] = sf[opp(i) * TN + l];
-    }
-    bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-    for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
   }
 }
 
@@ -445,35 +273,77 @@ k_step_tiles_s(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
 // 4 measured 0-7 % faster than 8 or 2 (profiles/ab_warps_per_block_r01.txt)
 constexpr int kWarpsPerBlock = LBM_WL_WARPS;
 
-// Warp work list (MODE 5/8): one warp per group of live bricks of one tile
-// (32 lanes = 4 fp32 / 8 fp64 bricks), so no lane idles for a tile's dead
-// bricks or its last partial pass and no CTA slot is held by a nearly empty
-// tile.  Each item is pre-decoded on the host: {tile, brick index per lane
-// group (bytes of words 1-2), uniform bits | count << 8}; the chain to the
-// data loads is item -> (nbr27, slot table, flags) -> data.  The 27
-// neighbour offsets live in lanes 0-26 and are fetched with shuffles.
-template <typename T, int TN, int MINB, bool SEL = false>
+// ------------------------------------------------------------------ TMA
+// Bulk-copy (TMA) primitives: 1-D cp.async.bulk global -> shared with
+// mbarrier transaction counting, and the L2 bulk prefetch.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+// one warp's share of the work list: {tile, brick index per lane group
+// (bytes of words 1-2), uniform bits | count << 8}, decoded on the host
+struct WarpItem {
+  int t, l;
+  bool in, uniform;
+  template <typename T>
+  __device__ __forceinline__ static WarpItem decode(const uint4 it, int lane, const Geo& g) {
+    WarpItem W;
+    const int lbn = g.lbx + g.lby + g.lbz;
+    const int gi = lane >> lbn;  // brick group of this lane
+    W.t = (int)it.x;
+    W.in = gi < (int)((it.w >> 8) & 15u);
+    const int b = (int)(((gi < 4 ? it.y : it.z) >> (8 * (gi & 3))) & 255u);
+    W.l = (b << lbn) | (lane & ((1 << lbn) - 1));
+    W.uniform = W.in && ((it.w >> gi) & 1u);
+    return W;
+  }
+};
+
+// Warp work list (the default for sparse tiles): one warp per group of
+// live bricks of one tile (32 lanes = 4 fp32 / 8 fp64 bricks), so no lane
+// idles for a tile's dead bricks and no CTA slot is held by a nearly empty
+// tile.  The chain to the data loads is item -> (nbr27, slot table, flags)
+// -> data.  Exact per-link select: masked links never fetch the upstream slot.
+// CUT: z-slab ghost exchange for items of tiles on the first / last tile plane.
+template <typename T, int TN, int MINB, bool CUT = false>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
 k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-               const uint4* __restrict__ items, int n_items, const unsigned long long* __restrict__ lut) {
+               const uint4* __restrict__ items, int n_items, const ulonglong2* __restrict__ lut,
+               const TileHalo<T> TH = TileHalo<T>{}) {
   const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
-  const uint4 it = __ldg(items + wid);
-  const int t = (int)it.x;
-  int srel = 0;
-  if (lane < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + lane);
-    srel = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
-  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  const int gi = lane >> lbn;  // brick group of this lane
-  const bool in = gi < (int)((it.w >> 8) & 15u);
-  const int b = (int)(((gi < 4 ? it.y : it.z) >> (8 * (gi & 3))) & 255u);
-  const int l = (b << lbn) | (lane & (bn - 1));
-  const bool uniform = in && ((it.w >> gi) & 1u);
-  const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
+  const WarpItem W = WarpItem::decode<T>(__ldg(items + wid), lane, g);
+  const int t = W.t, l = W.l;
+  const int srel = nbr_rel<T, TN>(nbr27, t, lane);
+  const uint32_t w = W.uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (W.in ? __ldg(flags + (size_t)t * TN + l) : 0u);
   const bool live = flag_type(w) != SOLID;
   const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
   const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
@@ -485,26 +355,35 @@ k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
 #pragma unroll
   for (int i = 1; i < Q; ++i) off[i] = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
   if (!live) {
-    if (zfill && in) {
+    if (zfill && W.in) {
 #pragma unroll
-      for (int i = 0; i < Q; ++i) tp[i * TN + l] = (T)0;
+      for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = (T)0;
     }
     return;
   }
   const uint32_t miss = ~w & kMaskBits;
   T f[Q];
-  f[0] = __ldg(tb + l);
+  f[0] = __ldg(tb + up.p);
 #pragma unroll
-  for (int i = 1; i < Q; ++i)  // SEL: masked links never fetch the (solid) upstream slot
-    f[i] = __ldg(tb + ((SEL && ((miss >> (opp(i) - 1)) & 1u)) ? opp(i) * TN + l : i * TN + off[i]));
-  if (!SEL && miss) {
-#pragma unroll
-    for (int i = 1; i < Q; ++i)
-      if ((miss >> (opp(i) - 1)) & 1u) f[i] = __ldg(tb + opp(i) * TN + l);
+  for (int i = 1; i < Q; ++i)
+    f[i] = __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + opp(i) * TN : off[i] + i * TN));
+  int x = 0, y = 0, z = -1;
+  bool cut = false;
+  if (CUT) {
+    const int tz0 = __ldg(TH.tiles + 3 * t + 2) * g.ez;
+    cut = tz0 == 0 || tz0 + g.ez >= g.nz;
+    if (cut) {
+      brick_inv(g, l, x, y, z);
+      x += __ldg(TH.tiles + 3 * t) * g.ex;
+      y += __ldg(TH.tiles + 3 * t + 1) * g.ey;
+      z += tz0;
+      tile_ghost_gather<T>(f, miss, TH, g, x, y, z);
+    }
   }
   bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) tp[i * TN + l] = f[i];
+  for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = f[i];
+  if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
 }
 
 // A-A in place over the tile list (see k_step_dense_aa for the scheme):
@@ -514,19 +393,13 @@ template <typename T, int TN, int NB, int MINB>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                 const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-                const uint32_t* __restrict__ bmask, const int* __restrict__ order,
-                const unsigned long long* __restrict__ lut) {
+                const uint32_t* __restrict__ bmask, const ulonglong2* __restrict__ lut) {
   constexpr int BT = TN < 256 ? TN : 256;
-  const int t = order ? __ldg(order + blockIdx.x) : (int)blockIdx.x;
+  const int t = blockIdx.x;
   const int lane = threadIdx.x & 31;
-  // neighbour ranks in lanes 0-26 (shuffles; no shared table, no barrier)
-  int srel = 0;
-  if (NB && lane < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + lane);
-    srel = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
+  const int srel = NB ? nbr_rel<T, TN>(nbr27, t, lane) : 0;
   T* __restrict__ tb = F + (size_t)t * (Q * TN);
-  const TileBricks tw(bmask, t, g, TN, true);
+  const TileBricks tw(bmask, t, g, TN);
 #pragma unroll 1
   for (int k = threadIdx.x - lane; k < tw.work; k += BT) {  // whole warps
     bool in;
@@ -535,12 +408,13 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
     const bool live = flag_type(w) != SOLID;  // no zero-fill under AA (see k_step_dense_aa)
     if (!NB) {
       if (!live) continue;
+      const int p = l;
       T f[Q];
 #pragma unroll
-      for (int i = 0; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
+      for (int i = 0; i < Q; ++i) f[i] = LDA(tb + p + i * TN);
       bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
+      for (int i = 0; i < Q; ++i) tb[p + opp(i) * TN] = f[i];
       continue;
     }
     // neighbour step: the whole warp stays converged (solid lanes compute on
@@ -550,22 +424,22 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
     T f[Q];
     {
       const TileUpLUT up(lut, l);
-      f[0] = live ? LDA(tb + l) : (T)0;
+      f[0] = live ? LDA(tb + up.p) : (T)0;
 #pragma unroll
       for (int i = 1; i < Q; ++i) {
         const int off = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
         // exact per-link select: a masked link reads the node's own F[i]
-        f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? i * TN + l : opp(i) * TN + off)) : (T)0;
+        f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + i * TN : off + opp(i) * TN)) : (T)0;
       }
     }
     bc_collide<T>(f, w, bcv, bcr, om);
     const int l2 = opaque(l);
     const TileUpLUT up2(lut, l2);
-    if (live) tb[l2] = f[0];
+    if (live) tb[up2.p] = f[0];
 #pragma unroll
     for (int i = 1; i < Q; ++i) {
       const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
-      if (live) tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + off] = f[i];
+      if (live) tb[((miss >> (i - 1)) & 1u) ? up2.p + opp(i) * TN : off + i * TN] = f[i];
     }
   }
 }
@@ -578,54 +452,170 @@ template <typename T, int TN, int NB, int MINB>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
 k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                   const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om, const uint4* __restrict__ items,
-                  int n_items, const unsigned long long* __restrict__ lut) {
+                  int n_items, const ulonglong2* __restrict__ lut) {
   const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
-  const uint4 it = __ldg(items + wid);
-  const int t = (int)it.x;
-  int srel = 0;
-  if (NB && lane < 27) {
-    const int v = __ldg(nbr27 + 27LL * t + lane);
-    srel = v < 0 ? 0 : (v - t) * (Q * TN);
-  }
-  const int lbn = g.lbx + g.lby + g.lbz, bn = 1 << lbn;
-  const int gi = lane >> lbn;
-  const bool in = gi < (int)((it.w >> 8) & 15u);
-  const int b = (int)(((gi < 4 ? it.y : it.z) >> (8 * (gi & 3))) & 255u);
-  const int l = (b << lbn) | (lane & (bn - 1));
-  const bool uniform = in && ((it.w >> gi) & 1u);
-  const uint32_t w = uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (in ? __ldg(flags + (size_t)t * TN + l) : 0u);
+  const WarpItem W = WarpItem::decode<T>(__ldg(items + wid), lane, g);
+  const int t = W.t, l = W.l;
+  const int srel = NB ? nbr_rel<T, TN>(nbr27, t, lane) : 0;
+  const uint32_t w = W.uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (W.in ? __ldg(flags + (size_t)t * TN + l) : 0u);
   const bool live = flag_type(w) != SOLID;
   T* __restrict__ tb = F + (size_t)t * (Q * TN);
   if (!NB) {
     if (!live) return;
+    const int p = l;
     T f[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) f[i] = LDA(tb + i * TN + l);
+    for (int i = 0; i < Q; ++i) f[i] = LDA(tb + p + i * TN);
     bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) tb[opp(i) * TN + l] = f[i];
+    for (int i = 0; i < Q; ++i) tb[p + opp(i) * TN] = f[i];
     return;
   }
   const uint32_t miss = ~w & kMaskBits;
   T f[Q];
   {
     const TileUpLUT up(lut, l);
-    f[0] = live ? LDA(tb + l) : (T)0;
+    f[0] = live ? LDA(tb + up.p) : (T)0;
 #pragma unroll
     for (int i = 1; i < Q; ++i) {
       const int off = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
-      f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? i * TN + l : opp(i) * TN + off)) : (T)0;
+      f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + i * TN : off + opp(i) * TN)) : (T)0;
     }
   }
   bc_collide<T>(f, w, bcv, bcr, om);
   const int l2 = opaque(l);
   const TileUpLUT up2(lut, l2);
-  if (live) tb[l2] = f[0];
+  if (live) tb[up2.p] = f[0];
 #pragma unroll
   for (int i = 1; i < Q; ++i) {
     const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
-    if (live) tb[((miss >> (i - 1)) & 1u) ? opp(i) * TN + l2 : i * TN + off] = f[i];
+    if (live) tb[((miss >> (i - 1)) & 1u) ? up2.p + opp(i) * TN : off + i * TN] = f[i];
+  }
+}
+
+// TMA-staged tiles (variant 9; the north star's "TMA tile staging"):
+// persistent CTAs walk the tile list (tile = blockIdx.x + k * gridDim.x)
+// through an S-stage ring of tile images in shared memory.  For each tile,
+// warp 0 arms the stage's mbarrier with the tile's live bytes and its lanes
+// issue one cp.async.bulk per (direction, run of consecutive live bricks) --
+// 19 copies of 2 KB for a full tile -- S - 1 tiles ahead of the compute, so
+// the tile's own data is in flight without registers or LSU slots.  Dead
+// bricks are never copied (their nodes are solid: masked links).  In-tile
+// pulls read the stage, pulls across the tile faces read global memory,
+// stores go straight to the post buffer.  Measured slower than the direct
+// kernels (profiles/sparse_r02.md): 8-16 warps per SM leave the face loads'
+// latency exposed, and every tile costs a CTA barrier.
+template <typename T, int TN>
+struct TmaCfg {
+  static constexpr int BN = Rec<T>::BN;
+  static constexpr int NB = TN / BN;                 // bricks per tile
+  static constexpr int STAGE = Q * TN;               // elements per stage (a tile image)
+  static constexpr int S = 2;
+  static constexpr int THREADS = 256;
+  static constexpr size_t SMEM = (size_t)S * STAGE * sizeof(T) + 16 * S;
+};
+
+template <typename T, int TN>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1)
+k_step_tiles_tma(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
+                 const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
+                 const uint32_t* __restrict__ bmask, const ulonglong2* __restrict__ lut, int n_tiles) {
+  using C = TmaCfg<T, TN>;
+  constexpr int BN = C::BN, S = C::S;
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  T* const stage0 = reinterpret_cast<T*>(tma_smem);
+  unsigned long long* const full = reinterpret_cast<unsigned long long*>(tma_smem + (size_t)S * C::STAGE * sizeof(T));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  // warp 0: arm stage (k % S) and copy the live bricks of this CTA's k-th tile
+  auto issue = [&](int k) {
+    const int t = blockIdx.x + k * gridDim.x;
+    if (t >= n_tiles) return;
+    const int s = k % S;
+    uint32_t m[4];
+    int live = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      m[q] = __ldg(bmask + 8LL * t + q);
+      live += __popc(m[q]);
+    }
+    if (lane == 0) mbar_expect_tx(&full[s], (unsigned)(live * Q * BN * (int)sizeof(T)));
+    __syncwarp();
+    const T* src = pre + (size_t)t * (Q * TN);
+    T* dst = stage0 + (size_t)s * C::STAGE;
+#pragma unroll
+    for (int q = 0; q < (C::NB + 31) / 32; ++q) {
+      // lane j starts a run if brick 32q + j is live and its predecessor in the word is not
+      const uint32_t mq = m[q];
+      const bool start = ((mq >> lane) & 1u) && (lane == 0 || !((mq >> (lane - 1)) & 1u));
+      if (start) {
+        const int len = __ffs(~(mq >> lane)) - 1;   // consecutive live bricks from lane
+        const int b0 = q * 32 + lane;
+        for (int i = 0; i < Q; ++i)
+          bulk_g2s(dst + i * TN + b0 * BN, src + i * TN + b0 * BN, (unsigned)(len * BN * sizeof(T)), &full[s]);
+      }
+    }
+  };
+  if (warp == 0)
+    for (int k = 0; k < S - 1; ++k) issue(k);
+#pragma unroll 1
+  for (int k = 0;; ++k) {
+    const int t = blockIdx.x + k * gridDim.x;
+    if (t >= n_tiles) break;
+    if (warp == 0) issue(k + S - 1);  // into the stage released at the end of k - 1
+    const int s = k % S;
+    const T* __restrict__ sb = stage0 + (size_t)s * C::STAGE;
+    const int srel = nbr_rel<T, TN>(nbr27, t, lane);
+    const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
+    T* __restrict__ tp = post + (size_t)t * (Q * TN);
+    const TileBricks tw(bmask, t, g, TN);
+    mbar_wait(&full[s], (unsigned)((k / S) & 1));
+#pragma unroll 1
+    for (int kk = threadIdx.x - lane; kk < tw.work; kk += C::THREADS) {  // whole warps
+      bool in;
+      const int l = tw.slot(kk + lane, in);
+      const uint32_t w = tw.flag(flags, t, TN, l, in);
+      const bool live = flag_type(w) != SOLID;
+      const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
+      const TileUpLUT up(lut, l);
+      int off[Q];
+      uint32_t intile = 0u;  // bit i: the node x - c_i lies in this tile (read the stage)
+#pragma unroll
+      for (int i = 1; i < Q; ++i) {
+        const int c = up.code(i), loc = up.loc(i);
+        const int rel = __shfl_sync(0xffffffffu, srel, c);  // all lanes take part
+        intile |= (c == 13 ? 1u : 0u) << i;
+        off[i] = c == 13 ? loc : rel + loc;
+      }
+      if (!live) {
+        if (zfill && in) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) tp[l + i * TN] = (T)0;
+        }
+        continue;
+      }
+      const uint32_t miss = ~w & kMaskBits;
+      T f[Q];
+      f[0] = sb[l];
+#pragma unroll
+      for (int i = 1; i < Q; ++i) {
+        if ((miss >> (opp(i) - 1)) & 1u)
+          f[i] = sb[l + opp(i) * TN];
+        else if ((intile >> i) & 1u)
+          f[i] = sb[off[i] + i * TN];
+        else
+          f[i] = __ldg(tb + off[i] + i * TN);
+      }
+      bc_collide<T>(f, w, bcv, bcr, om);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) tp[l + i * TN] = f[i];
+    }
+    __syncthreads();  // stage s is free again
   }
 }

@@ -168,9 +168,9 @@ def test_aa_fully_periodic_box_vs_oracle():
 
 @pytest.mark.parametrize("layout", ["tile", "pointer_tile"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("variant", ["8", "10"])
+@pytest.mark.parametrize("variant", ["8", "7"])
 def test_aa_tile_kernels_bitwise(monkeypatch, layout, dtype, variant):
-    """Both A-A tile kernels (warp work list: 8, one CTA per tile: 10) give
+    """Both A-A tile kernels (warp work list: 8, one CTA per tile: 7) give
     the oracle's state bit for bit in both phases."""
     monkeypatch.setenv("LBM_STEP_VARIANT", variant)
     c = random_mixed_geometry3(3, n=(24, 16, 16), periodic_z=True)

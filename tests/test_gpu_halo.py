@@ -36,7 +36,7 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     connect_local(sims, periodic_z)
     for s in sims:
         s.initialize(1.0)
-    for chunk in (1, 3, 16):
+    for chunk in (1, 3, 16, 40):   # 40: a 32-step CUDA-graph replay (wait / boundary / signal / interior)
         single.step(chunk)
         for s in sims:
             s.step(chunk, block=False)
@@ -49,7 +49,7 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     assert np.array_equal(fl, single.flag_words())
     ref = oracle_sim(c, params.omega, dtype)
     ref.initialize(1.0)
-    ref.step(20)
+    ref.step(single.step_count)
     assert np.array_equal(single.canonical_state(), ref.pre)
 
 
@@ -78,7 +78,7 @@ def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
     connect_local(sims, periodic_z)
     for s in sims:
         s.initialize(1.0)
-    for chunk in (1, 2, 13):
+    for chunk in (1, 2, 13, 40):
         single.step(chunk)
         for s in sims:
             s.step(chunk, block=False)
@@ -88,7 +88,7 @@ def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
         assert np.array_equal(got, single.canonical_state()), chunk
     ref = oracle_sim(c, params.omega, dtype)
     ref.initialize(1.0)
-    ref.step(16)
+    ref.step(single.step_count)
     assert np.array_equal(single.canonical_state(), ref.pre)
 
 

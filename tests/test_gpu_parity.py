@@ -331,33 +331,39 @@ def test_single_perturbed_node_matches_plain_loop_step():
 
 
 def test_launch_configuration_does_not_change_results(monkeypatch):
-    """Analogue of t/test_kernel.py:143-156 (worker count): every step-kernel
-    variant, tile launch order, tile shape and the CUDA-graph replay give
-    bitwise-identical states."""
+    """Analogue of t/test_kernel.py:143-156 (worker count): every tile kernel
+    (warp work list, CTA per tile, TMA-staged), every tile shape, the AB and
+    A-A schemes and the CUDA-graph replay reproduce the ORACLE bitwise."""
+    from oracle.step19 import OracleSim
     geom = lb.build_porous_random(40, 0.45, seed=5, radius_range=(3, 7), dims=(40, 32, 24))
     params = lb.FlowParams.from_viscosity(U=0.05, L=31, nu=0.2)
+    d = geom.descriptors
+    kinds, vel, rho = geom.boundary_values.as_arrays()
+    oracle = OracleSim(d.type_tag, d.orientation, d.bc_index, kinds, vel, rho, params.omega,
+                       dtype=np.float32, periodic=d.periodic)
+    oracle.initialize(1.005)
+    oracle.step(37)
 
-    def run(layout, tile=(8, 8, 8), **env):
-        for k in ("LBM_STEP_VARIANT", "LBM_TILE_ORDER", "LBM_GRAPH"):
+    def run(layout, tile=(8, 8, 8), scheme="ab", **env):
+        for k in ("LBM_STEP_VARIANT", "LBM_GRAPH"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
-        sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, tile=tile)
+        sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, tile=tile, scheme=scheme)
         sim.initialize(1.005)
         sim.step(37)
         return sim.canonical_state()
 
-    ref = run("dense", LBM_GRAPH="0")
-    for v in ("0", "1", "2", "3", "8"):
-        assert np.array_equal(run("dense", LBM_STEP_VARIANT=v), ref), v
-    for v in ("0", "1", "2", "3", "4", "5", "6", "7", "8", "10"):
-        assert np.array_equal(run("pointer_tile", LBM_STEP_VARIANT=v), ref), v
-    for order in ("morton", "pencil:2", "z:2"):
-        assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order), ref), order
-        # the work list follows the launch order too
-        assert np.array_equal(run("pointer_tile", LBM_TILE_ORDER=order, LBM_STEP_VARIANT="8"), ref), order
-    for tile in ((4, 8, 16), (16, 4, 8), (8, 4, 1)):
-        assert np.array_equal(run("pointer_tile", tile=tile), ref), tile
+    assert np.array_equal(run("dense", LBM_GRAPH="0"), oracle.pre)
+    assert np.array_equal(run("dense"), oracle.pre)
+    for scheme in ("ab", "aa"):
+        for v in ("7", "8", "9"):   # CTA per tile, warp work list, TMA-staged tiles
+            for tile in ((8, 8, 8), (4, 8, 16)):
+                got = run("pointer_tile", tile=tile, scheme=scheme, LBM_STEP_VARIANT=v)
+                assert np.array_equal(got, oracle.pre), (scheme, v, tile)
+    for tile in ((16, 4, 8), (8, 4, 1), (32, 2, 4)):
+        assert np.array_equal(run("pointer_tile", tile=tile), oracle.pre), tile
+        assert np.array_equal(run("tile", tile=tile), oracle.pre), tile
 
 
 def test_square_duct_profile_matches_analytic():
