@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblbm19.so")
+# LBM_LIB: an alternative build of the same ABI (the experiments library,
+# python -m paper_2108_13241_b200.build --experiments -> exp_lib/liblbm19_exp.so)
+LIB_PATH = os.environ.get("LBM_LIB") or os.path.join(_HERE, "_lib", "liblbm19.so")
 
 LBM_OK, LBM_EINVAL, LBM_ESTATE, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EDIVERGED = \
     0, -1, -2, -3, -4, -5, -6

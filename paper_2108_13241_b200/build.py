@@ -1,6 +1,11 @@
 """Build liblbm19.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
 
-    python -m paper_2108_13241_b200.build [--verbose]
+    python -m paper_2108_13241_b200.build [--verbose] [--experiments]
+
+--experiments builds exp_lib/liblbm19_exp.so with -DLBM_EXPERIMENTS: the
+measured-slower dense step variants (warp-uniform select, 128-bit vector
+kernel; LBM_STEP_VARIANT=1/2/3/8) next to the product kernels.  Load it with
+LBM_LIB=exp_lib/liblbm19_exp.so.  The product library never contains them.
 """
 import os
 import subprocess
@@ -27,19 +32,21 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, experiments=False):
+    lib = os.path.join(ROOT, "exp_lib", "liblbm19_exp.so") if experiments else LIB
+    if not force and not experiments and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + SOURCES + ["-o", LIB + ".tmp"]
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    cmd = [NVCC] + FLAGS + (["-DLBM_EXPERIMENTS"] if experiments else []) + \
+        (["-Xptxas", "-v"] if verbose else []) + SOURCES + ["-o", lib + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv))
+    print(build(force=True, verbose="--verbose" in sys.argv, experiments="--experiments" in sys.argv))

@@ -103,6 +103,7 @@ struct lbm_handle {
   uint32_t* items = nullptr;  // warp work list, 4 words per warp (tile, brick bytes x2, uniform | count), MODE 5/8
   unsigned long long* lut = nullptr;  // per in-tile slot neighbour deltas (TileUpLUT)
   int n_items = 0;
+  int n_items_b = 0;        // z-slabs: the first n_items_b items hold the boundary tile planes
   bool auto_wlist = false;  // default tile kernel = warp work list (sparse tiles)
   bool wlist_ok = false;    // work-list items fit their packing (<= 8 brick groups per warp)
   double live_frac = 1.0;   // live bricks / brick slots of the kept tiles
@@ -217,6 +218,7 @@ void free_geometry(lbm_handle* h) {
   dev_free(h->lut);
   h->lut = nullptr;
   h->n_items = 0;
+  h->n_items_b = 0;
   h->wlist_ok = h->auto_wlist = false;
   dev_free(h->gh[0]);
   dev_free(h->gh[1]);
@@ -350,8 +352,10 @@ void launch_tiles_tma(lbm_handle* h, const T* pre, T* post) {
       (const ulonglong2*)h->lut, (int)h->n_tiles);
 }
 
+// part (z-slabs on the work list): 0 every item, 1 the boundary tile planes
+// (with the ghost exchange), 2 the interior items
 template <typename T, int TN>
-void launch_tiles(lbm_handle* h, const T* pre, T* post) {
+void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
   constexpr int BT = TN < 256 ? TN : 256;
   const TileHalo<T> TH = make_tile_halo<T>(h, h->parity, 1 - h->parity);
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
@@ -373,8 +377,20 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post) {
   }
   if (wl) {
     if (!h->n_items) return;
-    const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const uint4* it = (const uint4*)h->items;
+    if (TH.on && part != 0) {
+      const int i0 = part == 1 ? 0 : h->n_items_b, n = part == 1 ? h->n_items_b : h->n_items - h->n_items_b;
+      if (n <= 0) return;
+      const unsigned nbk = (unsigned)((n + kWarpsPerBlock - 1) / kWarpsPerBlock);
+      if (part == 1)  // the ghost exchange needs 48 registers (fp32)
+        k_step_tiles_w<T, TN, MW * 5 / 6, true><<<nbk, 32 * kWarpsPerBlock, 0, h->stream>>>(
+            pre, post, h->flags, h->nbr27, bv, br, h->g, om, it + i0, n, lut, TH);
+      else
+        k_step_tiles_w<T, TN, MW><<<nbk, 32 * kWarpsPerBlock, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br,
+                                                                              h->g, om, it + i0, n, lut);
+      return;
+    }
+    const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
     if (TH.on)  // the ghost exchange needs 48 registers (fp32)
       k_step_tiles_w<T, TN, MW * 5 / 6, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
           pre, post, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, TH);
@@ -459,7 +475,7 @@ int launch_step(lbm_handle* h, const void* pre, void* post, int zmode = 0) {
       Halo<T> H = h->parity == 0 ? make_halo<T>(h, 0) : Halo<T>{};
       H.zmode = zmode;
       if (h->parity == 0)
-        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
+        k_step_dense_aa_nb<T, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
       else
         k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
     } else {
@@ -506,11 +522,11 @@ int launch_step(lbm_handle* h, const void* pre, void* post, int zmode = 0) {
   } else {
     if (h->n_tiles == 0) return 0;
     switch (g.tn) {
-      case 32: launch_tiles<T, 32>(h, (const T*)pre, (T*)post); break;
-      case 64: launch_tiles<T, 64>(h, (const T*)pre, (T*)post); break;
-      case 128: launch_tiles<T, 128>(h, (const T*)pre, (T*)post); break;
-      case 256: launch_tiles<T, 256>(h, (const T*)pre, (T*)post); break;
-      default: launch_tiles<T, 512>(h, (const T*)pre, (T*)post); break;
+      case 32: launch_tiles<T, 32>(h, (const T*)pre, (T*)post, zmode); break;
+      case 64: launch_tiles<T, 64>(h, (const T*)pre, (T*)post, zmode); break;
+      case 128: launch_tiles<T, 128>(h, (const T*)pre, (T*)post, zmode); break;
+      case 256: launch_tiles<T, 256>(h, (const T*)pre, (T*)post, zmode); break;
+      default: launch_tiles<T, 512>(h, (const T*)pre, (T*)post, zmode); break;
     }
   }
   h->launches += 1;
@@ -518,13 +534,17 @@ int launch_step(lbm_handle* h, const void* pre, void* post, int zmode = 0) {
 }
 
 // one step of a connected z-slab: wait for the neighbours' previous step,
-// then (dense) the two boundary planes, the signal, and the interior -- the
-// neighbours' next step overlaps this slab's interior; tile slabs signal
-// after the whole step
+// then the boundary planes (dense) / boundary tile planes (work list), the
+// signal, and the interior -- the neighbours' next step overlaps this slab's
+// interior.  Safe because only boundary-plane threads touch the ghost planes
+// (AB) or the neighbour's boundary plane (A-A), and the signal follows them.
 template <typename T>
 void slab_step(lbm_handle* h, const void* pre, void* post) {
   halo_wait(h);
-  if (!h->g.tiled) {
+  // dense (AB and A-A) always; tile slabs when they run the work list (its
+  // items are ordered boundary tile planes first)
+  const bool split = !h->g.tiled || (!h->g.aa && h->wlist_ok && (h->variant_set ? h->variant == 8 : h->auto_wlist));
+  if (split) {
     launch_step<T>(h, pre, post, 1);
     halo_signal(h);
     launch_step<T>(h, pre, post, 2);
@@ -553,7 +573,7 @@ void preload_halo_kernels(const lbm_handle* h) {
   cudaFuncGetAttributes(&a, k_halo_wait);
   cudaFuncGetAttributes(&a, k_halo_signal);
   if (!h->g.tiled && h->g.aa) {
-    cudaFuncGetAttributes(&a, k_step_dense_aa<T, 1, D1>);
+    cudaFuncGetAttributes(&a, k_step_dense_aa_nb<T, D1>);
     cudaFuncGetAttributes(&a, k_step_dense_aa<T, 0, D1>);
   } else if (!h->g.tiled) {
     cudaFuncGetAttributes(&a, k_halo_push<T>);
@@ -1133,6 +1153,23 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
               rec[3] |= (uint32_t)k << 8;
               it.insert(it.end(), rec, rec + 4);
             }
+          }
+          // z-slabs: items of the first / last tile plane first (they hold the
+          // ghost exchange), so the step can signal its neighbours before the
+          // interior items run
+          h->n_items_b = 0;
+          if ((h->has_glo || h->has_ghi) && !it.empty() && T > 0) {
+            std::vector<int> tz((size_t)T * 3);
+            CK(scopy(h, tz.data(), h->tiles, (size_t)T * 12, cudaMemcpyDeviceToHost));
+            std::vector<uint32_t> bnd, inner;
+            for (size_t k = 0; k < it.size(); k += 4) {
+              const int z3 = tz[3 * (size_t)it[k] + 2];
+              auto& dst = (z3 == 0 || z3 == g.gz - 1) ? bnd : inner;
+              dst.insert(dst.end(), it.begin() + k, it.begin() + k + 4);
+            }
+            h->n_items_b = (int)(bnd.size() / 4);
+            bnd.insert(bnd.end(), inner.begin(), inner.end());
+            it.swap(bnd);
           }
           pt.mark("brick masks to host + work list");
           h->n_items = (int)(it.size() / 4);
@@ -1751,8 +1788,8 @@ int lbm_get_stats(lbm_t* h, lbm_stats* s) {
   s->parity = h->parity;
   s->initialized = h->initialized ? 1 : 0;
   s->scheme = h->d.scheme;
-  // z-slab tile handles (ghost planes) run the CTA-per-tile exchange kernel
-  s->tile_work_list = h->gh[0] == nullptr && h->wlist_ok &&
+  // (z-slab tile handles run the work list with the ghost exchange compiled in)
+  s->tile_work_list = h->wlist_ok &&
       ((h->auto_wlist && !h->variant_set) || (h->g.tiled && h->variant == 8)) ? 1 : 0;
   return 0;
 }

@@ -159,6 +159,10 @@ struct UpOffsets {
     zm = (z == 0 && g.pzw) ? (unsigned)(g.nz - 1) * pl : 0u - pl;
     zp = (z == g.nz - 1 && g.pzw) ? 0u - (unsigned)(g.nz - 1) * pl : pl;
   }
+  // slot of (x, y - cy_i, z - cz_i): the y / z part of up()
+  __device__ __forceinline__ unsigned up_yz(unsigned s, int i) const {
+    return s + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0u)) + (cz(i) == 1 ? zm : (cz(i) == -1 ? zp : 0u));
+  }
   // slot of x - c_i
   __device__ __forceinline__ unsigned up(unsigned s, int i) const {
     return s + (cx(i) == 1 ? xm : (cx(i) == -1 ? xp : 0u)) + (cy(i) == 1 ? ym : (cy(i) == -1 ? yp : 0u)) +
@@ -449,5 +453,121 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
     bc_collide<T>(f, w, bcv, bcr, om);
 #pragma unroll
     for (int i = 0; i < Q; ++i) P.f[opp(i)][s] = f[i];
+  }
+}
+
+// A-A neighbour step (phase 0 -> 1) with row-aligned pushes.  The ten
+// directions with c_x != 0 push to x + c_i, one element off the warp's
+// 128-B line: every such warp store wrote 2 partial sectors (read-modify-
+// write in L2).  Here a node hands those values through shared memory to
+// the thread of its CTA that owns column x + c_x, which stores the whole
+// row segment aligned -- only the CTA's two edge columns and periodic wraps
+// store directly.  Same pulls, arithmetic and single-owner locations as
+// k_step_dense_aa<NB = 1>, so the result is bitwise the same.
+// the directions with c_x != 0: 1 3 5 6 7 8 11 12 13 14
+__host__ __device__ constexpr int kXShift(int j) { return j < 2 ? 1 + 2 * j : (j < 6 ? j + 3 : j + 5); }
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_step_dense_aa_nb(const Planes1<T> P, const uint32_t* __restrict__ flags,
+                                                         const uint32_t* __restrict__ ubits,
+                                                         const T* __restrict__ bcv, const T* __restrict__ bcr,
+                                                         Geo g, T om, const Halo<T> H) {
+  __shared__ T shv[10][128];
+  __shared__ uint32_t shm[128];  // bit j: this column pushes kXShift(j) through shv
+  const int tid = threadIdx.x;
+  const int x = blockIdx.x * 128 + tid;
+  const int y = blockIdx.y, z = slab_z(blockIdx.z, H.zmode, g.nz);
+  const bool valid = x < g.nx;   // padding columns take part in the barrier only
+  const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + (valid ? x : 0);
+  const unsigned s = fi + (unsigned)g.plane;
+  uint32_t w = 0u;
+  if (valid) {
+    const uint32_t ub = __ldg(ubits + (fi >> 10));
+    w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  }
+  const bool live = valid && flag_type(w) != SOLID;
+  const uint32_t miss = ~w & kMaskBits;
+  uint32_t pushm = 0u;
+  if (live) {
+    T f[Q];
+    f[0] = LDA(P.f[0] + s);
+    {
+      const UpOffsets o(g, x, y, z);
+#pragma unroll
+      for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));  // speculative, always a valid slot
+    }
+    if (miss) {
+#pragma unroll
+      for (int i = 1; i < Q; ++i)
+        if ((miss >> (opp(i) - 1)) & 1u) f[i] = LDA(P.f[i] + s);
+    }
+    const bool top = z == g.nz - 1 && H.hi[0], bot = z == 0 && H.lo[0];
+    if (top || bot) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (top) {
+          const int i = kZm(j);
+          if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = H.hi[j][peer_row<T>(g, x - cx(i), y - cy(i))];
+        }
+        if (bot) {
+          const int i = kZp(j);
+          if (!((miss >> (opp(i) - 1)) & 1u)) f[i] = H.lo[j][peer_row<T>(g, x - cx(i), y - cy(i))];
+        }
+      }
+    }
+    bc_collide<T>(f, w, bcv, bcr, om);
+    const unsigned s2 = opaque(s);
+    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
+    P.f[0][s2] = f[0];
+    int jx = 0;
+#pragma unroll
+    for (int i = 1; i < Q; ++i) {
+      if ((miss >> (i - 1)) & 1u) {
+        P.f[opp(i)][s2] = f[i];  // masked: own slot
+      } else if (cx(i) == 0) {
+        P.f[i][o2.up(s2, opp(i))] = f[i];  // x + c_i in the same column: aligned
+      } else {
+        const int xt = x + cx(i), tt = tid + cx(i);
+        if (xt >= 0 && xt < g.nx && tt >= 0 && tt < 128) {
+          shv[jx][tid] = f[i];
+          pushm |= 1u << jx;
+        } else {
+          P.f[i][o2.up(s2, opp(i))] = f[i];  // CTA edge or periodic wrap: direct
+        }
+      }
+      if (cx(i) != 0) ++jx;
+    }
+    if (top || bot) {
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (top) {
+          const int i = kZp(j);
+          if ((miss >> (i - 1)) & 1u) continue;
+          H.hi[j][peer_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        if (bot) {
+          const int i = kZm(j);
+          if ((miss >> (i - 1)) & 1u) continue;
+          H.lo[j][peer_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+        }
+      }
+      __threadfence_system();
+    }
+  }
+  shm[tid] = pushm;
+  __syncthreads();
+  if (!valid) return;
+  // receive: column x stores, for each x-shifted direction, the value pushed
+  // by x - c_x of the same row into row (y + c_y, z + c_z) -- one aligned
+  // 128-B line per warp
+  const UpOffsets o3(g, x, y, z);
+#pragma unroll
+  for (int j = 0; j < 10; ++j) {
+    const int i = kXShift(j);
+    const int ts = tid - cx(i);
+    if (ts >= 0 && ts < 128 && ((shm[ts] >> j) & 1u)) P.f[i][o3.up_yz(s, opp(i))] = shv[j][ts];
   }
 }

@@ -555,7 +555,8 @@ k_step_tiles_tma(const T* __restrict__ pre, T* __restrict__ post, const uint32_t
       const uint32_t mq = m[q];
       const bool start = ((mq >> lane) & 1u) && (lane == 0 || !((mq >> (lane - 1)) & 1u));
       if (start) {
-        const int len = __ffs(~(mq >> lane)) - 1;   // consecutive live bricks from lane
+        const uint32_t rest = ~(mq >> lane);         // zeros shifted in above bit 31 - lane
+        const int len = rest ? __ffs(rest) - 1 : 32;  // consecutive live bricks from lane (32: a full word)
         const int b0 = q * 32 + lane;
         for (int i = 0; i < Q; ++i)
           bulk_g2s(dst + i * TN + b0 * BN, src + i * TN + b0 * BN, (unsigned)(len * BN * sizeof(T)), &full[s]);

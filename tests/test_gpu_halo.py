@@ -60,10 +60,17 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     ("tile", (8, 8, 4), 2, True, np.float32),
     ("pointer_tile", (8, 8, 8), 2, False, np.float64),
     ("pointer_tile", (4, 8, 16), 2, False, np.float32),
-    ("pointer_tile", (8, 8, 8), 3, True, np.float32)])
-def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype):
+    ("pointer_tile", (8, 8, 8), 3, True, np.float32),
+    ("pointer_tile", (4, 8, 16), 2, True, "wl"),
+    ("pointer_tile", (8, 8, 8), 3, False, "wl")])
+def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype, monkeypatch):
     """Sparse z-slabs: cuts on tile planes balanced by non-solid count; the
-    boundary tiles exchange through ghost planes inside the step kernel."""
+    boundary tiles exchange through ghost planes inside the step kernel.
+    "wl": the warp work list (forced), whose slab steps run the boundary tile
+    planes' items first, signal, then the interior items."""
+    if dtype == "wl":
+        monkeypatch.setenv("LBM_STEP_VARIANT", "8")
+        dtype = np.float32
     c = random_mixed_geometry3(13, n=(19, 12, 24), periodic_z=periodic_z)
     geom = to_geometry(c)
     params = _params(1.25)
