@@ -18,42 +18,41 @@ __device__ __forceinline__ uint32_t type_at(const uint8_t* __restrict__ type,
     if (!g.py) return SOLID;
     y = y < 0 ? y + g.ny : y - g.ny;
   }
-  if (z < 0) return glo ? glo[(long long)y * g.nx + x] : SOLID;
-  if (z >= g.nz) return ghi ? ghi[(long long)y * g.nx + x] : SOLID;
-  return type[((long long)z * g.ny + y) * g.nx + x];
+  if (z < 0) return glo ? glo[(long long)y * g.nx + x] & 7u : SOLID;
+  if (z >= g.nz) return ghi ? ghi[(long long)y * g.nx + x] & 7u : SOLID;
+  return type[((long long)z * g.ny + y) * g.nx + x] & 7u;
 }
 
+// descriptors as uploaded (packed and range-checked on the host, lbm19.cu
+// upload_descriptors): type | orientation << 3, and the bc index byte
 __device__ __forceinline__ uint32_t node_flag(const uint8_t* __restrict__ type,
-                                              const uint8_t* __restrict__ orient,
-                                              const int* __restrict__ bcidx,
+                                              const uint8_t* __restrict__ bcb,
                                               const uint8_t* __restrict__ glo,
                                               const uint8_t* __restrict__ ghi, const Geo& g,
-                                              int x, int y, int z, int nb, int* err) {
+                                              int x, int y, int z) {
   const long long n = ((long long)z * g.ny + y) * g.nx + x;
-  const uint32_t t = type[n];
-  const uint32_t o = orient[n];
-  const int b = bcidx[n];
-  if (t > PRESSURE_BC || o > O_BOTTOM) atomicOr(err, 1);
-  if ((t == VELOCITY_BC || t == PRESSURE_BC) && (b < 0 || b >= nb || o == O_NONE)) atomicOr(err, 2);
+  const uint32_t t = type[n] & 7u;
+  const uint32_t o = type[n] >> 3;
+  const uint32_t b = bcb[n];
   uint32_t m = 0;
   if (t != SOLID) {
 #pragma unroll
     for (int j = 1; j < Q; ++j)
       if (type_at(type, glo, ghi, g, x + cx(j), y + cy(j), z + cz(j)) != SOLID) m |= 1u << (j - 1);
   }
-  return make_flag(m, t, o, b < 0 ? 0u : (uint32_t)b);
+  return make_flag(m, t, o, b);
 }
 
 // dense: one thread per (padded) flag entry
 __global__ void k_flags_dense(uint32_t* __restrict__ flags, const uint8_t* __restrict__ type,
-                              const uint8_t* __restrict__ orient, const int* __restrict__ bcidx,
+                              const uint8_t* __restrict__ bcb,
                               const uint8_t* __restrict__ glo, const uint8_t* __restrict__ ghi,
-                              Geo g, int nb, int* err, unsigned long long* nonsolid) {
+                              Geo g, unsigned long long* nonsolid) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y, z = blockIdx.z;
   if (x >= g.nxp) return;
   uint32_t w = 0;
-  if (x < g.nx) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
+  if (x < g.nx) w = node_flag(type, bcb, glo, ghi, g, x, y, z);
   flags[((long long)z * g.ny + y) * g.nxp + x] = w;
   const unsigned c = __popc(__ballot_sync(0xffffffffu, flag_type(w) != SOLID));
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(nonsolid, (unsigned long long)c);
@@ -73,7 +72,7 @@ __global__ void k_tile_keep(int* __restrict__ keep, const uint8_t* __restrict__ 
     for (int l = lane; l < g.tn && !any; l += 32) {
       const int lx = l & (g.ex - 1), ly = (l >> g.lex) & (g.ey - 1), lz = l >> (g.lex + g.ley);
       const int x = tx * g.ex + lx, y = ty * g.ey + ly, z = tz * g.ez + lz;
-      if (x < g.nx && y < g.ny && z < g.nz && type[((long long)z * g.ny + y) * g.nx + x] != SOLID) any = 1;
+      if (x < g.nx && y < g.ny && z < g.nz && (type[((long long)z * g.ny + y) * g.nx + x] & 7u) != SOLID) any = 1;
     }
     any = __any_sync(0xffffffffu, any);
   }
@@ -116,10 +115,10 @@ __global__ void k_tile_nbr(int* __restrict__ nbr, const int* __restrict__ tiles,
 
 // tiles: one thread per slot of the kept tiles
 __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict__ tiles,
-                             const uint8_t* __restrict__ type, const uint8_t* __restrict__ orient,
-                             const int* __restrict__ bcidx, const uint8_t* __restrict__ glo,
-                             const uint8_t* __restrict__ ghi, Geo g, long long nslots, int nb,
-                             int* err, unsigned long long* nonsolid) {
+                             const uint8_t* __restrict__ type, const uint8_t* __restrict__ bcb,
+                             const uint8_t* __restrict__ glo,
+                             const uint8_t* __restrict__ ghi, Geo g, long long nslots,
+                             unsigned long long* nonsolid) {
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t w = 0;
   if (s < nslots) {
@@ -130,7 +129,7 @@ __global__ void k_flags_tile(uint32_t* __restrict__ flags, const int* __restrict
     const int x = tiles[3 * t] * g.ex + lx;
     const int y = tiles[3 * t + 1] * g.ey + ly;
     const int z = tiles[3 * t + 2] * g.ez + lz;
-    if (x < g.nx && y < g.ny && z < g.nz) w = node_flag(type, orient, bcidx, glo, ghi, g, x, y, z, nb, err);
+    if (x < g.nx && y < g.ny && z < g.nz) w = node_flag(type, bcb, glo, ghi, g, x, y, z);
     flags[s] = w;
   }
   const unsigned c = __popc(__ballot_sync(0xffffffffu, s < nslots && flag_type(w) != SOLID));

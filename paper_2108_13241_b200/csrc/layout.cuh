@@ -84,9 +84,23 @@ struct SlotMap {
 //   phase 1 (odd):             pre_i(x) = F[i][x + c_i] if link i of x is
 //                              present, else F[opp(i)][x]
 // (see k_step_dense_aa for the two steps that produce these states).
+// Tile A-A z-slabs: a present link across the cut has x + c_i in the
+// neighbouring slab; the neighbour step mirrored that push into the region
+// appended to this slab's buffer (offset Q * ps, step_tiles.cuh TileAAHalo).
 __device__ __forceinline__ long long pre_index(const Geo& g, const SlotMap& sm, int i, long long s,
                                                uint32_t w, int x, int y, int z) {
   if (!g.aa || i == 0) return fidx(g, i, s);
-  if (g.aph && ((w >> (i - 1)) & 1u)) return fidx(g, i, sm.nbr_slot(g, x, y, z, i));
+  if (g.aph && ((w >> (i - 1)) & 1u)) {
+    const int zz = z + cz(i);
+    if (g.tiled && !g.pzw && (zz < 0 || zz >= g.nz)) {
+      int xx = x + cx(i), yy = y + cy(i);
+      if (xx < 0) xx += g.nx; else if (xx >= g.nx) xx -= g.nx;
+      if (yy < 0) yy += g.ny; else if (yy >= g.ny) yy -= g.ny;
+      const long long pn = (long long)g.nx * g.ny;
+      const int j = zz < 0 ? (i - 10) / 2 : 5 + (i - 9) / 2;  // kZm(j) -> j, kZp(j) -> 5 + j
+      return (long long)Q * g.ps + j * pn + (long long)yy * g.nx + xx;
+    }
+    return fidx(g, i, sm.nbr_slot(g, x, y, z, i));
+  }
   return fidx(g, opp(i), s);
 }

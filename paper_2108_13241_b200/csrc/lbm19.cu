@@ -136,6 +136,7 @@ struct lbm_handle {
   struct Peer {
     bool on = false, ipc = false;
     void* f[2] = {nullptr, nullptr};
+    int* rank = nullptr;   // tile A-A slabs: the neighbour's tile rank grid (peer memory)
     unsigned long long* sync = nullptr;
     long long ps = 0;
     int nz = 0;
@@ -244,8 +245,12 @@ void free_geometry(lbm_handle* h) {
 
 bool is_tiled(int layout) { return layout == LBM_LAYOUT_TILE || layout == LBM_LAYOUT_POINTER_TILE; }
 
-// elements of one PDF buffer: 19 planes of ps (tiles: T tiles x 19 blocks)
-long long buf_elems(const lbm_handle* h) { return (long long)Q * h->g.ps; }
+// elements of one PDF buffer: 19 planes of ps (tiles: T tiles x 19 blocks),
+// plus, on tile A-A z-slabs, the 2 x 5 mirror planes of the cross-cut pushes
+long long buf_elems(const lbm_handle* h) {
+  const bool mirror = h->g.tiled && h->g.aa && (h->has_glo || h->has_ghi);
+  return (long long)Q * h->g.ps + (mirror ? 10LL * h->g.nx * h->g.ny : 0LL);
+}
 
 dim3 node_grid(const Geo& g, int bx) { return dim3((g.nx + bx - 1) / bx, g.ny, g.nz); }
 
@@ -406,6 +411,25 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
     k_step_tiles_x<T, TN, M><<<nt, BT, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
 }
 
+template <typename T>
+TileAAHalo<T> make_tile_aa_halo(const lbm_handle* h) {
+  TileAAHalo<T> AH{};
+  const Geo& g = h->g;
+  const long long row = (long long)g.gy * g.gx;
+  if (h->lo.on) {
+    AH.f_lo = (T*)h->lo.f[0];
+    AH.rank_lo = h->lo.rank + (long long)((h->lo.nz - 1) >> g.lez) * row;
+    AH.lz_lo = (h->lo.nz - 1) & (g.ez - 1);
+  }
+  if (h->hi.on) {
+    AH.f_hi = (T*)h->hi.f[0];
+    AH.rank_hi = h->hi.rank;  // its tile plane 0
+  }
+  AH.mirror = (T*)h->f[0] + (size_t)Q * g.ps;
+  AH.tiles = h->tiles;
+  return AH;
+}
+
 template <typename T, int TN>
 void launch_tiles_aa(lbm_handle* h, T* F) {
   constexpr int BT = TN < 256 ? TN : 256;
@@ -425,7 +449,10 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
     // 48 resident warps for both phases (40 registers; the neighbour step
     // spills 8 B and still measured 0-1 % faster than 40 warps at 48
     // registers, profiles/ab_aa_warp_list_r01.txt)
-    if (h->parity == 0)
+    if (h->parity == 0 && halo_on(h))  // z-slab: the cut's links reach into the neighbours
+      k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 2, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
+          F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, make_tile_aa_halo<T>(h));
+    else if (h->parity == 0)
       k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
           F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut);
     else
@@ -433,7 +460,10 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
           F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut);
     return;
   }
-  if (h->parity == 0)
+  if (h->parity == 0 && halo_on(h))
+    k_step_tiles_aa<T, TN, 1, (MN * 5 / 6 > 0 ? MN * 5 / 6 : 1), true><<<nt, BT, 0, h->stream>>>(
+        F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut, make_tile_aa_halo<T>(h));
+  else if (h->parity == 0)
     k_step_tiles_aa<T, TN, 1, MN><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
   else
     k_step_tiles_aa<T, TN, 0, M><<<nt, BT, 0, h->stream>>>(F, h->flags, h->nbr27, bv, br, h->g, om, h->bmask, lut);
@@ -474,9 +504,14 @@ int launch_step(lbm_handle* h, const void* pre, void* post, int zmode = 0) {
       if (grid.z == 0) return 0;
       Halo<T> H = h->parity == 0 ? make_halo<T>(h, 0) : Halo<T>{};
       H.zmode = zmode;
-      if (h->parity == 0)
-        k_step_dense_aa_nb<T, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
-      else
+      if (h->parity == 0) {
+#ifdef LBM_EXPERIMENTS
+        if (h->variant == 12)  // row-aligned pushes through shared memory (measured slower)
+          k_step_dense_aa_nb<T, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
+        else
+#endif
+        k_step_dense_aa<T, 1, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
+      } else
         k_step_dense_aa<T, 0, D1><<<grid, 128, 0, h->stream>>>(F, h->flags, h->ubits, bv, br, g, om, H);
     } else {
       if (h->n_tiles == 0) return 0;
@@ -562,6 +597,12 @@ template <typename T, int TN>
 void preload_tiles(cudaFuncAttributes* a) {
   constexpr int BT = TN < 256 ? TN : 256;
   constexpr int M = sizeof(T) == 4 ? (1536 / BT > 32 ? 32 : 1536 / BT) : (768 / BT);
+  constexpr int MN = M * 5 / 6 > 0 ? M * 5 / 6 : 1;
+  cudaFuncGetAttributes(a, k_step_tiles_aa<T, TN, 1, (MN * 5 / 6 > 0 ? MN * 5 / 6 : 1), true>);
+  cudaFuncGetAttributes(a, k_step_tiles_aa<T, TN, 0, M>);
+  cudaFuncGetAttributes(a, k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 2, true>);
+  cudaFuncGetAttributes(a, k_step_tiles_aa_w<T, TN, 0, sizeof(T) == 4 ? 6 : 3>);
+  cudaFuncGetAttributes(a, k_step_tiles_w<T, TN, sizeof(T) == 4 ? 6 : 3>);
   cudaFuncGetAttributes(a, k_step_tiles_x<T, TN, (M * 5 / 6 > 0 ? M * 5 / 6 : 1), true, true>);
   cudaFuncGetAttributes(a, k_step_tiles_w<T, TN, (sizeof(T) == 4 ? 6 : 3) * 5 / 6, true>);
 }
@@ -573,7 +614,7 @@ void preload_halo_kernels(const lbm_handle* h) {
   cudaFuncGetAttributes(&a, k_halo_wait);
   cudaFuncGetAttributes(&a, k_halo_signal);
   if (!h->g.tiled && h->g.aa) {
-    cudaFuncGetAttributes(&a, k_step_dense_aa_nb<T, D1>);
+    cudaFuncGetAttributes(&a, k_step_dense_aa<T, 1, D1>);
     cudaFuncGetAttributes(&a, k_step_dense_aa<T, 0, D1>);
   } else if (!h->g.tiled) {
     cudaFuncGetAttributes(&a, k_halo_push<T>);
@@ -716,6 +757,68 @@ static int pipelined_h2d(lbm_handle* h, void* dev, const void* host, size_t byte
     CK(cudaMemcpyAsync((char*)dev + off, h->pin[b], len, cudaMemcpyHostToDevice, h->stream));
     CK(cudaEventRecord(h->evc[b], h->stream));
   }
+  return 0;
+}
+
+// Descriptor upload packed on the host: type | orientation << 3 and the bc
+// index byte (the flag word keeps 8 bits of it) -- 2 B per node on the wire
+// instead of 6 -- range-checked while packing (threads), each chunk's DMA
+// overlapping the packing of the next through the two pinned slots.
+// err: bit 0 type / orientation out of range, bit 1 a velocity / pressure
+// node without a valid bc index or orientation.
+static int upload_descriptors(lbm_handle* h, uint8_t* dto, uint8_t* dbc, const uint8_t* type, const uint8_t* orient,
+                              const int32_t* bc, long long N, int nb, int* err) {
+  const size_t half = 32u << 20;  // nodes per chunk: 32 MB of each output per pinned slot
+  if (h->pin_bytes < 2 * half) {
+    for (int b = 0; b < 2; ++b) {
+      if (h->pin[b]) cudaFreeHost(h->pin[b]);
+      h->pin[b] = nullptr;
+    }
+    h->pin_bytes = 0;
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc(&h->pin[b], 2 * half, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", 2 * half);
+      }
+    h->pin_bytes = 2 * half;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
+  static const int hw = [] {
+    const unsigned c = std::thread::hardware_concurrency();
+    return c == 0 ? 8 : (c > 16 ? 16 : (int)c);
+  }();
+  std::vector<int> errs(hw, 0);
+  const long long nchunk = (N + (long long)half - 1) / (long long)half;
+  for (long long k = 0; k < nchunk; ++k) {
+    const int b = (int)(k & 1);
+    const long long off = k * (long long)half, n = N - off < (long long)half ? N - off : (long long)half;
+    CK(cudaEventSynchronize(h->evc[b]));  // slot b's previous DMA is done
+    uint8_t* pto = (uint8_t*)h->pin[b];
+    uint8_t* pbc = pto + half;
+    const int nt = n > (1 << 20) ? hw : 1;
+    auto work = [&](int t) {
+      const long long per = (n + nt - 1) / nt, a = per * t, e = a + per < n ? a + per : n;
+      int er = 0;
+      for (long long i = a; i < e; ++i) {
+        const uint32_t ty = type[off + i], o = orient[off + i];
+        const int32_t bi = bc[off + i];
+        er |= (ty > PRESSURE_BC || o > O_BOTTOM) ? 1 : 0;
+        er |= ((ty == VELOCITY_BC || ty == PRESSURE_BC) && (bi < 0 || bi >= nb || o == O_NONE)) ? 2 : 0;
+        pto[i] = (uint8_t)((ty & 7u) | (o & 7u) << 3);
+        pbc[i] = bi < 0 ? 0 : (uint8_t)bi;
+      }
+      errs[t] |= er;
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    CK(cudaMemcpyAsync(dto + off, pto, (size_t)n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(dbc + off, pbc, (size_t)n, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaEventRecord(h->evc[b], h->stream));
+  }
+  for (int e : errs) *err |= e;
   return 0;
 }
 
@@ -927,6 +1030,7 @@ void lbm_destroy(lbm_t* h) {
       cudaIpcCloseMemHandle(pr->f[0]);
       if (pr->f[1] != pr->f[0]) cudaIpcCloseMemHandle(pr->f[1]);
       cudaIpcCloseMemHandle(pr->sync);
+      if (pr->rank) cudaIpcCloseMemHandle(pr->rank);
     }
     pr->on = false;
   }
@@ -981,21 +1085,21 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
   const long long N = h->n_nodes;
   const long long plane_nodes = (long long)g.nx * g.ny;
   int rc = 0;
-  uint8_t *dtype_ = nullptr, *dorient = nullptr, *dglo = nullptr, *dghi = nullptr;
-  int* dbc = nullptr;
+  uint8_t *dtype_ = nullptr, *dorient = nullptr, *dglo = nullptr, *dghi = nullptr;  // dtype_: type | orient << 3
+  uint8_t* dbc = nullptr;  // bc index byte
+  int herr_host = 0;
   int* derr = nullptr;
   int *keep = nullptr, *scan = nullptr;
   void* cub_tmp = nullptr;
   const int nbt = nb > 0 ? nb : 1;
   PhaseTimer pt(h->stream);
   // temporaries
-  if ((rc = dev_alloc(h, &dtype_, N)) || (rc = dev_alloc(h, &dorient, N)) ||
-      (rc = dev_alloc(h, &dbc, N * 4)) || (rc = dev_alloc(h, &derr, 16)))
+  if ((rc = dev_alloc(h, &dtype_, N)) || (rc = dev_alloc(h, &dbc, N)) || (rc = dev_alloc(h, &derr, 16)))
     goto done;
   pt.mark("alloc temporaries");
-  if ((rc = pipelined_h2d(h, dtype_, type, N)) || (rc = pipelined_h2d(h, dorient, orient, N)) ||
-      (rc = pipelined_h2d(h, dbc, bc_index, N * 4)))
-    goto done;
+  if ((rc = upload_descriptors(h, dtype_, dbc, type, orient, bc_index, N, nb, &herr_host))) goto done;
+  if (herr_host & 1) { rc = fail(LBM_EINVAL, "node type or orientation out of range"); goto done; }
+  if (herr_host & 2) { rc = fail(LBM_EINVAL, "velocity/pressure node without a valid bc_index or orientation"); goto done; }
   CK(cudaMemsetAsync(derr, 0, 16, h->stream));
   CK(cudaMemsetAsync(h->uscratch, 0, 4 * sizeof(unsigned long long), h->stream));
   h->has_glo = ghost_lo != nullptr;  // z-slab: links cross z = -1 / z = nz into a neighbour
@@ -1044,8 +1148,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     if (!g.tiled) {
       if ((rc = dev_alloc(h, &h->flags, h->nflags * 4))) goto done;
       dim3 grid((g.nxp + 127) / 128, g.ny, g.nz);
-      k_flags_dense<<<grid, 128, 0, h->stream>>>(h->flags, dtype_, dorient, dbc, glo, ghi, g, nb, derr,
-                                                 h->uscratch);
+      k_flags_dense<<<grid, 128, 0, h->stream>>>(h->flags, dtype_, dbc, glo, ghi, g, h->uscratch);
       CKL();
       const long long nwords = (h->nflags + 1023) / 1024;
       if ((rc = dev_alloc(h, &h->ubits, nwords * 4))) goto done;
@@ -1101,7 +1204,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       if (h->nflags > 0) {
         pt.mark("compact + nbr27 + order");
         k_flags_tile<<<(unsigned)((h->nflags + 255) / 256), 256, 0, h->stream>>>(
-            h->flags, h->tiles, dtype_, dorient, dbc, glo, ghi, g, h->nflags, nb, derr, h->uscratch);
+            h->flags, h->tiles, dtype_, dbc, glo, ghi, g, h->nflags, h->uscratch);
         CKL();
       }
       if ((rc = dev_alloc(h, &h->bmask, (T > 0 ? T : 1) * 32))) goto done;
@@ -1219,8 +1322,9 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
         if ((rc = dev_alloc(h, &h->lut, lt.size() * 8))) goto done;
         CK(scopy(h, h->lut, lt.data(), lt.size() * 8, cudaMemcpyHostToDevice));
       }
-      // z-slab ghost planes (tile layouts keep them outside the tile storage)
-      if (h->has_glo || h->has_ghi) {
+      // z-slab ghost planes (AB tile layouts keep them outside the tile
+      // storage; A-A tile slabs reach into the neighbour directly)
+      if ((h->has_glo || h->has_ghi) && !g.aa) {
         const size_t gb = (size_t)10 * plane_nodes * h->esize;
         if ((rc = dev_alloc(h, (char**)&h->gh[0], gb)) || (rc = dev_alloc(h, (char**)&h->gh[1], gb))) goto done;
         CK(cudaMemsetAsync(h->gh[0], 0, gb, h->stream));
@@ -1677,7 +1781,7 @@ static int field_io(lbm_t* h, int which, void* host, bool get) {
   if (!h->geometry) return fail(LBM_ESTATE, "no geometry");
   if (h->g.aa && which != 0) return fail(LBM_EINVAL, "the AA scheme keeps one buffer: there is no post buffer");
   DeviceGuard dg(h->d.device);
-  const size_t bytes = (size_t)buf_elems(h) * h->esize;
+  const size_t bytes = (size_t)Q * h->g.ps * h->esize;
   if (h->g.aa) {
     // decoded pre buffer in the native slot order, staged on the device
     void* d = nullptr;
@@ -1799,11 +1903,14 @@ namespace {
 struct HaloBlob {
   uint32_t magic;
   int32_t device, esize, nz, ny, nxp, tiled, aa;
+  int32_t ex, ey, ez, gz;   // tile shape and tile-grid depth (tile layouts)
   int64_t pid, ps;
   void* f[2];
   void* sync;
+  void* rank;               // tile A-A slabs: the tile rank grid
   cudaIpcMemHandle_t ipc_f[2];
   cudaIpcMemHandle_t ipc_sync;
+  cudaIpcMemHandle_t ipc_rank;
 };
 constexpr uint32_t kHaloMagic = 0x4C424D48u;  // "LBMH"
 static_assert(sizeof(HaloBlob) <= LBM_HALO_BLOB_BYTES, "halo blob too large");
@@ -1811,8 +1918,9 @@ static_assert(sizeof(HaloBlob) <= LBM_HALO_BLOB_BYTES, "halo blob too large");
 int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
   if (b.magic != kHaloMagic) return fail(LBM_EINVAL, "not a halo blob");
   if (b.esize != h->esize || b.ny != h->g.ny || b.nxp != h->g.nxp || b.tiled != h->g.tiled ||
-      b.aa != h->g.aa)
-    return fail(LBM_EINVAL, "neighbouring slab has a different dtype, layout family or x/y extent");
+      b.aa != h->g.aa || (h->g.tiled && (b.ex != h->g.ex || b.ey != h->g.ey || b.ez != h->g.ez)))
+    return fail(LBM_EINVAL, "neighbouring slab has a different dtype, layout family, tile shape or x/y extent");
+  const bool tile_aa = h->g.tiled && h->g.aa;
   if (b.pid == (int64_t)getpid()) {
     if (b.device != h->d.device) {
       int can = 0;
@@ -1826,6 +1934,7 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
     pr.f[0] = b.f[0];
     pr.f[1] = b.f[1];
     pr.sync = (unsigned long long*)b.sync;
+    pr.rank = tile_aa ? (int*)b.rank : nullptr;
     pr.ipc = false;
   } else {
     CK(cudaIpcOpenMemHandle(&pr.f[0], b.ipc_f[0], cudaIpcMemLazyEnablePeerAccess));
@@ -1836,6 +1945,11 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
     void* sy = nullptr;
     CK(cudaIpcOpenMemHandle(&sy, b.ipc_sync, cudaIpcMemLazyEnablePeerAccess));
     pr.sync = (unsigned long long*)sy;
+    if (tile_aa) {
+      void* rk = nullptr;
+      CK(cudaIpcOpenMemHandle(&rk, b.ipc_rank, cudaIpcMemLazyEnablePeerAccess));
+      pr.rank = (int*)rk;
+    }
     pr.ipc = true;
   }
   pr.ps = b.ps;
@@ -1848,8 +1962,8 @@ int open_peer(lbm_handle* h, const HaloBlob& b, lbm_handle::Peer& pr) {
 int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_export");
-  if (h->g.aa && h->g.tiled) return fail(LBM_EINVAL, "A-A z-slabs need a dense layout in this build");
-  if (h->g.tiled && !h->gh[0]) return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
+  if (h->g.tiled && !h->has_glo && !h->has_ghi)
+    return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
   DeviceGuard dg(h->d.device);
   HaloBlob b;
   memset(&b, 0, sizeof(b));
@@ -1863,8 +1977,18 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
   b.ps = h->g.ps;
   b.tiled = h->g.tiled;
   b.aa = h->g.aa;
-  // dense: the PDF buffers (ghost planes inside); tiles: the ghost-plane buffers
-  void* const* ex = h->g.tiled ? h->gh : h->f;
+  b.ex = h->g.ex;
+  b.ey = h->g.ey;
+  b.ez = h->g.ez;
+  b.gz = h->g.gz;
+  // dense: the PDF buffers (ghost planes inside); AB tiles: the ghost-plane
+  // buffers; A-A tiles: the tile storage itself and its rank grid
+  const bool tile_aa = h->g.tiled && h->g.aa;
+  void* const* ex = (h->g.tiled && !tile_aa) ? h->gh : h->f;
+  if (tile_aa) {
+    b.rank = h->rank;
+    CK(cudaIpcGetMemHandle(&b.ipc_rank, h->rank));
+  }
   b.f[0] = ex[0];
   b.f[1] = ex[1] ? ex[1] : ex[0];  // A-A: one buffer
   b.sync = h->sync;
@@ -1880,7 +2004,7 @@ int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes) {
 int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   if (!h->geometry) return fail(LBM_ESTATE, "lbm_set_geometry must run before lbm_halo_connect");
-  if (h->g.tiled && !h->gh[0] && (lo_blob || hi_blob))
+  if (h->g.tiled && !h->has_glo && !h->has_ghi && (lo_blob || hi_blob))
     return fail(LBM_EINVAL, "this tile handle is not a z-slab (no ghost planes)");
   if (h->g.pzw && (lo_blob || hi_blob))
     return fail(LBM_EINVAL, "a whole-domain periodic handle wraps z itself; it takes no halo");

@@ -456,6 +456,7 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
   }
 }
 
+#ifdef LBM_EXPERIMENTS
 // A-A neighbour step (phase 0 -> 1) with row-aligned pushes.  The ten
 // directions with c_x != 0 push to x + c_i, one element off the warp's
 // 128-B line: every such warp store wrote 2 partial sectors (read-modify-
@@ -463,7 +464,9 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
 // the thread of its CTA that owns column x + c_x, which stores the whole
 // row segment aligned -- only the CTA's two edge columns and periodic wraps
 // store directly.  Same pulls, arithmetic and single-owner locations as
-// k_step_dense_aa<NB = 1>, so the result is bitwise the same.
+// k_step_dense_aa<NB = 1>, so the result is bitwise the same.  Measured
+// 8 % SLOWER on C2 (0.81 vs 0.887 of the roofline, profiles/aa_r02.md): the
+// barrier and 12 B of spills cost more than the partial sectors it removes.
 // the directions with c_x != 0: 1 3 5 6 7 8 11 12 13 14
 __host__ __device__ constexpr int kXShift(int j) { return j < 2 ? 1 + 2 * j : (j < 6 ? j + 3 : j + 5); }
 
@@ -571,3 +574,4 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa_nb(const Planes1<T>
     if (ts >= 0 && ts < 128 && ((shm[ts] >> j) & 1u)) P.f[i][o3.up_yz(s, opp(i))] = shv[j][ts];
   }
 }
+#endif  // LBM_EXPERIMENTS

@@ -386,14 +386,98 @@ k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
 }
 
+// A-A z-slabs for tile layouts: like the dense A-A slabs, the neighbour
+// step of a boundary node reads and writes the neighbouring slab's boundary
+// plane directly in ITS tile storage (peer memory; its rank grid row of that
+// tile plane locates the node), and mirrors the pushes into a 2 x 5-plane
+// region appended to this slab's own buffer (offset Q * ps), where the
+// phase-1 readback decoder (pre_index) finds them.  The node-local step needs
+// nothing: the neighbour's pushes land in this slab's storage.
+template <typename T>
+struct TileAAHalo {
+  T* f_lo;             // lower neighbour's tile storage (its top plane is plane lz_lo of tile plane row rank_lo)
+  T* f_hi;             // upper neighbour's tile storage (its plane 0)
+  const int* rank_lo;  // (gy, gx) ranks of the lower neighbour's top tile plane
+  const int* rank_hi;  // (gy, gx) ranks of the upper neighbour's bottom tile plane
+  int lz_lo;           // in-tile z of the lower neighbour's top plane
+  T* mirror;           // own buffer + Q * ps: [kZm(j) x plane | kZp(j) x plane]
+  const int* tiles;    // own tile coordinates
+};
+
+// element of direction d at node (x, y, plane lz of the given tile-plane row)
+template <typename T>
+__device__ __forceinline__ long long peer_tile_elem(const Geo& g, const int* __restrict__ rank_row, int x, int y,
+                                                    int lz, int d) {
+  if (x < 0) x += g.nx; else if (x >= g.nx) x -= g.nx;  // present links wrap only on periodic axes
+  if (y < 0) y += g.ny; else if (y >= g.ny) y -= g.ny;
+  const long long r = __ldg(rank_row + (y >> g.ley) * g.gx + (x >> g.lex));
+  const int l = brick_x(g, x & (g.ex - 1)) + brick_y(g, y & (g.ey - 1)) + brick_z(g, lz);
+  return (r * Q + d) * g.tn + l;
+}
+
+// pulls of a boundary node across the cut (replacing the meaningless values
+// the in-slab gather produced for those links)
+template <typename T>
+__device__ __forceinline__ void tile_aa_cut_pull(T (&f)[Q], uint32_t miss, const TileAAHalo<T>& AH, const Geo& g,
+                                                 int x, int y, int z) {
+  if (z == 0 && AH.f_lo) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZp(j);  // c_z = +1: x - c_i is the lower neighbour's top plane, stored at F[opp(i)]
+      if (!((miss >> (opp(i) - 1)) & 1u))
+        f[i] = AH.f_lo[peer_tile_elem<T>(g, AH.rank_lo, x - cx(i), y - cy(i), AH.lz_lo, opp(i))];
+    }
+  }
+  if (z == g.nz - 1 && AH.f_hi) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZm(j);
+      if (!((miss >> (opp(i) - 1)) & 1u))
+        f[i] = AH.f_hi[peer_tile_elem<T>(g, AH.rank_hi, x - cx(i), y - cy(i), 0, opp(i))];
+    }
+  }
+}
+
+// is push i of a node at z a cross-cut push (stored by tile_aa_cut_push, not in-slab)?
+template <typename T>
+__device__ __forceinline__ bool tile_aa_cut_link(const TileAAHalo<T>& AH, const Geo& g, int z, int i) {
+  return (cz(i) == -1 && z == 0 && AH.f_lo) || (cz(i) == 1 && z == g.nz - 1 && AH.f_hi);
+}
+
+template <typename T>
+__device__ __forceinline__ void tile_aa_cut_push(const T (&f)[Q], uint32_t miss, const TileAAHalo<T>& AH,
+                                                 const Geo& g, int x, int y, int z) {
+  const long long pn = (long long)g.nx * g.ny;
+  if (z == 0 && AH.f_lo) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZm(j);
+      if ((miss >> (i - 1)) & 1u) continue;
+      AH.f_lo[peer_tile_elem<T>(g, AH.rank_lo, x + cx(i), y + cy(i), AH.lz_lo, i)] = f[i];
+      AH.mirror[j * pn + ghost_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+    }
+  }
+  if (z == g.nz - 1 && AH.f_hi) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const int i = kZp(j);
+      if ((miss >> (i - 1)) & 1u) continue;
+      AH.f_hi[peer_tile_elem<T>(g, AH.rank_hi, x + cx(i), y + cy(i), 0, i)] = f[i];
+      AH.mirror[(5 + j) * pn + ghost_row<T>(g, x + cx(i), y + cy(i))] = f[i];
+    }
+  }
+  __threadfence_system();
+}
+
 // A-A in place over the tile list (see k_step_dense_aa for the scheme):
 // NB = 1 pulls F[opp(i)] at x - c_i and pushes to F[i] at x + c_i through
 // the neighbour table; NB = 0 is node-local.
-template <typename T, int TN, int NB, int MINB>
+template <typename T, int TN, int NB, int MINB, bool CUT = false>
 __global__ void __launch_bounds__(TN < 256 ? TN : 256, MINB)
 k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                 const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-                const uint32_t* __restrict__ bmask, const ulonglong2* __restrict__ lut) {
+                const uint32_t* __restrict__ bmask, const ulonglong2* __restrict__ lut,
+                const TileAAHalo<T> AH = TileAAHalo<T>{}) {
   constexpr int BT = TN < 256 ? TN : 256;
   const int t = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -432,6 +516,14 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
         f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + i * TN : off + opp(i) * TN)) : (T)0;
       }
     }
+    int x = 0, y = 0, z = -1;
+    if (CUT) {
+      brick_inv(g, l, x, y, z);
+      x += __ldg(AH.tiles + 3 * t) * g.ex;
+      y += __ldg(AH.tiles + 3 * t + 1) * g.ey;
+      z += __ldg(AH.tiles + 3 * t + 2) * g.ez;
+      if (live) tile_aa_cut_pull<T>(f, miss, AH, g, x, y, z);
+    }
     bc_collide<T>(f, w, bcv, bcr, om);
     const int l2 = opaque(l);
     const TileUpLUT up2(lut, l2);
@@ -439,8 +531,11 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
 #pragma unroll
     for (int i = 1; i < Q; ++i) {
       const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
-      if (live) tb[((miss >> (i - 1)) & 1u) ? up2.p + opp(i) * TN : off + i * TN] = f[i];
+      const bool own = (miss >> (i - 1)) & 1u;
+      if (live && (own || !CUT || !tile_aa_cut_link<T>(AH, g, z, i)))
+        tb[own ? up2.p + opp(i) * TN : off + i * TN] = f[i];
     }
+    if (CUT && live) tile_aa_cut_push<T>(f, miss, AH, g, x, y, z);
   }
 }
 
@@ -448,11 +543,11 @@ k_step_tiles_aa(T* __restrict__ F, const uint32_t* __restrict__ flags, const int
 // work as k_step_tiles_aa, one warp per group of live bricks.  Any work
 // distribution is race-free under A-A: a node reads and writes only its own
 // slots (L) or the slots F[i][x + c_i] that only it reads (NB).
-template <typename T, int TN, int NB, int MINB>
+template <typename T, int TN, int NB, int MINB, bool CUT = false>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
 k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const int* __restrict__ nbr27,
                   const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om, const uint4* __restrict__ items,
-                  int n_items, const ulonglong2* __restrict__ lut) {
+                  int n_items, const ulonglong2* __restrict__ lut, const TileAAHalo<T> AH = TileAAHalo<T>{}) {
   const int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (wid >= n_items) return;  // whole warps
@@ -484,6 +579,14 @@ k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const i
       f[i] = live ? LDA(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + i * TN : off + opp(i) * TN)) : (T)0;
     }
   }
+  int x = 0, y = 0, z = -1;
+  if (CUT) {
+    brick_inv(g, l, x, y, z);
+    x += __ldg(AH.tiles + 3 * t) * g.ex;
+    y += __ldg(AH.tiles + 3 * t + 1) * g.ey;
+    z += __ldg(AH.tiles + 3 * t + 2) * g.ez;
+    if (live) tile_aa_cut_pull<T>(f, miss, AH, g, x, y, z);
+  }
   bc_collide<T>(f, w, bcv, bcr, om);
   const int l2 = opaque(l);
   const TileUpLUT up2(lut, l2);
@@ -491,8 +594,11 @@ k_step_tiles_aa_w(T* __restrict__ F, const uint32_t* __restrict__ flags, const i
 #pragma unroll
   for (int i = 1; i < Q; ++i) {
     const int off = __shfl_sync(0xffffffffu, srel, up2.code(opp(i))) + up2.loc(opp(i));  // x + c_i
-    if (live) tb[((miss >> (i - 1)) & 1u) ? up2.p + opp(i) * TN : off + i * TN] = f[i];
+    const bool own = (miss >> (i - 1)) & 1u;
+    if (live && (own || !CUT || !tile_aa_cut_link<T>(AH, g, z, i)))
+      tb[own ? up2.p + opp(i) * TN : off + i * TN] = f[i];
   }
+  if (CUT && live) tile_aa_cut_push<T>(f, miss, AH, g, x, y, z);
 }
 
 // TMA-staged tiles (variant 9; the north star's "TMA tile staging"):

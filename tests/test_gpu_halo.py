@@ -61,7 +61,7 @@ def test_slabs_in_process_bitwise(nslab, periodic_z, dtype):
     ("pointer_tile", (8, 8, 8), 2, False, np.float64),
     ("pointer_tile", (4, 8, 16), 2, False, np.float32),
     ("pointer_tile", (8, 8, 8), 3, True, np.float32),
-    ("pointer_tile", (4, 8, 16), 2, True, "wl"),
+    ("pointer_tile", (8, 4, 8), 2, True, "wl"),
     ("pointer_tile", (8, 8, 8), 3, False, "wl")])
 def test_tile_slabs_in_process_bitwise(layout, tile, nslab, periodic_z, dtype, monkeypatch):
     """Sparse z-slabs: cuts on tile planes balanced by non-solid count; the
@@ -133,6 +133,43 @@ def test_aa_slabs_in_process_bitwise(nslab, periodic_z, dtype):
         sims[0].set_state(sims[0].canonical_state())
 
 
+@pytest.mark.parametrize("tile,nslab,periodic_z,dtype,variant", [
+    ((8, 4, 4), 2, False, np.float32, None), ((8, 4, 4), 3, True, np.float64, None),
+    ((4, 8, 8), 2, True, np.float32, "8"), ((8, 8, 8), 3, False, np.float32, "8"),
+    ((4, 4, 2), 4, True, np.float32, "7")])
+def test_aa_tile_slabs_in_process_bitwise(tile, nslab, periodic_z, dtype, variant, monkeypatch):
+    """A-A z-slabs of pointer tiles: the neighbour step reaches into the
+    neighbouring slab's tile storage through its rank grid (peer memory) and
+    mirrors its cross-cut pushes for the phase-1 readback; CTA-per-tile and
+    work-list kernels, odd and even step counts, graph replay (37 steps), vs
+    the single-domain AB run, bitwise."""
+    if variant:
+        monkeypatch.setenv("LBM_STEP_VARIANT", variant)
+    c = random_mixed_geometry3(15, n=(19, 12, 24), periodic_z=periodic_z)
+    geom = to_geometry(c)
+    params = _params(1.2)
+    single = lb.Simulation(geom, params, scalar=dtype)
+    single.initialize(1.0)
+    sims = []
+    for z0, z1 in split_z_balanced(geom.descriptors.type_tag, nslab, align=tile[2]):
+        g, spec = slab_geometry(geom, z0, z1)
+        sims.append(lb.Simulation(g, params, layout="pointer_tile", scalar=dtype, tile=tile, slab=spec,
+                                  scheme="aa"))
+    connect_local(sims, periodic_z)
+    for s in sims:
+        s.initialize(1.0)
+    for chunk in (1, 2, 1, 37):
+        single.step(chunk)
+        for s in sims:
+            s.step(chunk, block=False)
+        for s in sims:
+            s.synchronize()
+        got = np.concatenate([s.canonical_state() for s in sims], axis=1)
+        assert np.array_equal(got, single.canonical_state()), (chunk, single.step_count)
+        rho = np.concatenate([s.macroscopic_fields()[0] for s in sims], axis=0)
+        assert np.array_equal(rho, single.macroscopic_fields()[0])
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -161,7 +198,7 @@ def _ipc_worker(rank, world, port, out_dir, layout="dense"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("layout", ["dense", "pointer_tile", "dense-aa"])
+@pytest.mark.parametrize("layout", ["dense", "pointer_tile", "dense-aa", "pointer_tile-aa"])
 def test_slabs_two_processes_ipc_bitwise(tmp_path, layout):
     import torch.multiprocessing as mp
     mp.spawn(_ipc_worker, args=(2, _free_port(), str(tmp_path), layout), nprocs=2, join=True)
