@@ -931,8 +931,6 @@ int lbm_create(const lbm_desc* desc, lbm_t** out) {
       if (d.periodic[a] && n3[a] % d.tile[a])
         return fail(LBM_EINVAL, "periodic axis %d needs extent %d divisible by the tile edge %d", a, n3[a], d.tile[a]);
   }
-  if (d.scheme == LBM_SCHEME_AA && nzg != d.nz && is_tiled(d.layout))
-    return fail(LBM_EINVAL, "the AA scheme is single-slab for tile layouts in this build");
   int ndev = 0;
   CK(cudaGetDeviceCount(&ndev));
   if (d.device < 0 || d.device >= ndev) return fail(LBM_EINVAL, "device %d not present (%d devices)", d.device, ndev);

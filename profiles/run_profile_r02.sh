@@ -17,4 +17,7 @@ LBM_STEP_VARIANT=9 timeout 900 bash profiles/profile.sh ${TAG}tma porous512
 LBM_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
   --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 50 --warmup 5 \
   > gpurun_out/bench_${TAG}_multi2_samegpu.json 2> gpurun_out/bench_${TAG}_multi2_samegpu.err
-ls -la gpurun_out
+
+# keep the copy-back under gpurun's 64 MiB: the raw/source CSVs carry the numbers
+rm -f gpurun_out/*.ncu-rep
+du -sh gpurun_out
