@@ -226,15 +226,19 @@ class ClockSampler:
 CPU_SLAB_NZ = 32   # the CPU sample: 512 x 512 x 32 z-periodic slab of C2
 
 
-def _cpu_port_sim():
+def _cpu_port_sim(duct=False):
     import numba
 
     from oracle.step19 import OracleSim
     import paper_2108_13241_b200 as lb
     cores = len(os.sched_getaffinity(0))
     numba.set_num_threads(cores)
-    geom = lb.build_channel(512, 512, CPU_SLAB_NZ, lb.VelocityInlet((0.05, 0.0, 0.0)))
-    omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25).omega
+    if duct:   # the multi-GPU workload (C5 duct): a 1024 x 1024 x 8 slab of it
+        geom = lb.build_duct_z(1024, 1024, CPU_SLAB_NZ // 4)
+        omega = lb.FlowParams.from_viscosity(U=0.05, L=1023, nu=0.1).omega
+    else:
+        geom = lb.build_channel(512, 512, CPU_SLAB_NZ, lb.VelocityInlet((0.05, 0.0, 0.0)))
+        omega = lb.FlowParams.from_viscosity(U=0.05, L=511, nu=0.25).omega
     d = geom.descriptors
     kinds, vel, rho = geom.boundary_values.as_arrays()
     sim = OracleSim(d.type_tag, d.orientation, d.bc_index, kinds, vel, rho, omega,
@@ -243,9 +247,10 @@ def _cpu_port_sim():
     return sim, int(np.count_nonzero(d.type_tag)), cores
 
 
-def _cpu_protocol(steps, warmup):
-    return (f"one protocol for both arms: 512x512x{CPU_SLAB_NZ} z-periodic slab of the C2 channel "
-            f"(same per-node work as C2), fp32, Numba port of the reference kernel (oracle/step19.py) "
+def _cpu_protocol(steps, warmup, duct=False):
+    where = (f"1024x1024x{CPU_SLAB_NZ // 4} slab of the C5 duct (same per-node work as C5)" if duct else
+             f"512x512x{CPU_SLAB_NZ} z-periodic slab of the C2 channel (same per-node work as C2)")
+    return (f"one protocol for both arms: {where}, fp32, Numba port of the reference kernel (oracle/step19.py) "
             f"parallel over rows with numba threads = host cores; {warmup} warm-up step(s) (JIT), then "
             f"{steps} steps timed as one continuous wall-clock region")
 
@@ -267,19 +272,22 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # each timed step = one step of the CPU port on the sample slab
-    sim, nons, cores = _cpu_port_sim()
+    # each timed step = one step of the CPU port on the sample slab of the
+    # workload our arm runs at this N (C2 at N = 1, the C5 duct at N > 1)
+    duct = int(os.environ.get("WORLD_SIZE", str(args.gpus))) > 1
+    sim, nons, cores = _cpu_port_sim(duct)
     sim.step(max(args.warmup, 1))
     t0 = time.perf_counter()
     sim.step(args.steps)
     dt = time.perf_counter() - t0
     v = nons * args.steps / dt / 1e6
-    sample = _cpu_protocol(args.steps, max(args.warmup, 1))
+    sample = _cpu_protocol(args.steps, max(args.warmup, 1), duct)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "MLUPS",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 channel 512^3 (CPU sample slab)", "sample_nodes": nons},
+            "config": {"workload": ("C5 duct 1024x1024x(256 N) (CPU sample slab)" if duct else
+                                    "C2 channel 512^3 (CPU sample slab)"), "sample_nodes": nons},
             "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0,
@@ -382,7 +390,9 @@ def main():
                            scheme=scheme, tile=tile)
         t_setup = time.perf_counter() - t0
         s2.initialize(rho0)
+        t_init = time.perf_counter()
         s2.step(args.steps)
+        t_step = time.perf_counter()
         fields = s2.density_field() if big else s2.macroscopic_fields()
         t1 = time.perf_counter()
         e2e = {"value": nons * args.steps / (t1 - t0) / 1e6, "unit": "MLUPS",
@@ -392,7 +402,9 @@ def main():
                           "macroscopic_fields() [f64 rho,u readback]") + ", wall clock",
                # the device geometry pipeline: descriptor upload, flag words,
                # tile keep/scan/compaction/nbr27, brick masks
-               "setup_s": t_setup, "setup_mnodes_per_s": nx * ny * nz / t_setup / 1e6}
+               "setup_s": t_setup, "setup_mnodes_per_s": nx * ny * nz / t_setup / 1e6,
+               "init_s": t_init - t0 - t_setup, "step_s": t_step - t_init, "readback_s": t1 - t_step,
+               "readback_gbs": d2h / (t1 - t_step) / 1e9}
         del fields
         s2.close()
 

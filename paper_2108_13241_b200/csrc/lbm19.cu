@@ -28,6 +28,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -375,7 +376,7 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
   // < 0.85 the warp work list with exact per-link select; fuller tiles one
   // CTA per tile with speculative gathers + bounce-back fix-up.  z-slabs run
   // the same kernels with the ghost-plane exchange compiled in.
-  const bool wl = h->wlist_ok && (h->variant_set ? h->variant == 8 : h->auto_wlist);
+  const bool wl = h->wlist_ok && (h->variant_set ? (h->variant == 8 || h->variant == 13) : h->auto_wlist);
   if (h->variant_set && h->variant == 9 && tma_ok(h)) {
     launch_tiles_tma<T, TN>(h, pre, post);
     return;
@@ -396,6 +397,18 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
       return;
     }
     const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (!TH.on && h->variant_set && h->variant == 13) {  // persistent warps, next item prefetched
+      static int per_sm = 0, sms = 0;
+      if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tiles_wp<T, TN, MW * 5 / 6>, 32 * kWarpsPerBlock, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->d.device);
+        if (per_sm < 1) per_sm = 1;
+      }
+      const unsigned grid = (unsigned)std::min<long long>((long long)per_sm * sms, nb);
+      k_step_tiles_wp<T, TN, MW * 5 / 6><<<grid, 32 * kWarpsPerBlock, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br,
+                                                                             h->g, om, it, h->n_items, lut);
+      return;
+    }
     if (TH.on)  // the ghost exchange needs 48 registers (fp32)
       k_step_tiles_w<T, TN, MW * 5 / 6, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
           pre, post, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, TH);
@@ -799,16 +812,25 @@ static int upload_descriptors(lbm_handle* h, uint8_t* dto, uint8_t* dbc, const u
     const int nt = n > (1 << 20) ? hw : 1;
     auto work = [&](int t) {
       const long long per = (n + nt - 1) / nt, a = per * t, e = a + per < n ? a + per : n;
-      int er = 0;
+      // branch-free so that the loop vectorises (host code is built with -O3)
+      const uint8_t* __restrict__ ty_ = type + off;
+      const uint8_t* __restrict__ or_ = orient + off;
+      const int32_t* __restrict__ bc_ = bc + off;
+      uint8_t* __restrict__ to_ = pto;
+      uint8_t* __restrict__ bb_ = pbc;
+      const uint32_t unb = (uint32_t)nb;
+      uint32_t er = 0;
       for (long long i = a; i < e; ++i) {
-        const uint32_t ty = type[off + i], o = orient[off + i];
-        const int32_t bi = bc[off + i];
-        er |= (ty > PRESSURE_BC || o > O_BOTTOM) ? 1 : 0;
-        er |= ((ty == VELOCITY_BC || ty == PRESSURE_BC) && (bi < 0 || bi >= nb || o == O_NONE)) ? 2 : 0;
-        pto[i] = (uint8_t)((ty & 7u) | (o & 7u) << 3);
-        pbc[i] = bi < 0 ? 0 : (uint8_t)bi;
+        const uint32_t ty = ty_[i], o = or_[i];
+        const int32_t bi = bc_[i];
+        const uint32_t isbc = (ty - (uint32_t)VELOCITY_BC) <= 1u;  // VELOCITY_BC or PRESSURE_BC
+        const uint32_t badb = (uint32_t)bi >= unb;                  // also bi < 0
+        er |= (uint32_t)(ty > (uint32_t)PRESSURE_BC) | (uint32_t)(o > (uint32_t)O_BOTTOM) |
+              ((isbc & (badb | (uint32_t)(o == (uint32_t)O_NONE))) << 1);
+        to_[i] = (uint8_t)((ty & 7u) | ((o & 7u) << 3));
+        bb_[i] = (uint8_t)(bi & ~(bi >> 31));                       // bc byte, negative -> 0
       }
-      errs[t] |= er;
+      errs[t] |= (int)er;
     };
     std::vector<std::thread> th;
     for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
@@ -1096,6 +1118,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     goto done;
   pt.mark("alloc temporaries");
   if ((rc = upload_descriptors(h, dtype_, dbc, type, orient, bc_index, N, nb, &herr_host))) goto done;
+  pt.mark("upload descriptors (packed)");
   if (herr_host & 1) { rc = fail(LBM_EINVAL, "node type or orientation out of range"); goto done; }
   if (herr_host & 2) { rc = fail(LBM_EINVAL, "velocity/pressure node without a valid bc_index or orientation"); goto done; }
   CK(cudaMemsetAsync(derr, 0, 16, h->stream));
