@@ -29,6 +29,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -376,7 +377,7 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
   // < 0.85 the warp work list with exact per-link select; fuller tiles one
   // CTA per tile with speculative gathers + bounce-back fix-up.  z-slabs run
   // the same kernels with the ghost-plane exchange compiled in.
-  const bool wl = h->wlist_ok && (h->variant_set ? (h->variant == 8 || h->variant == 13) : h->auto_wlist);
+  const bool wl = h->wlist_ok && (h->variant_set ? h->variant == 8 : h->auto_wlist);
   if (h->variant_set && h->variant == 9 && tma_ok(h)) {
     launch_tiles_tma<T, TN>(h, pre, post);
     return;
@@ -397,18 +398,6 @@ void launch_tiles(lbm_handle* h, const T* pre, T* post, int part = 0) {
       return;
     }
     const unsigned nb = (unsigned)((h->n_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    if (!TH.on && h->variant_set && h->variant == 13) {  // persistent warps, next item prefetched
-      static int per_sm = 0, sms = 0;
-      if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_tiles_wp<T, TN, MW * 5 / 6>, 32 * kWarpsPerBlock, 0);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->d.device);
-        if (per_sm < 1) per_sm = 1;
-      }
-      const unsigned grid = (unsigned)std::min<long long>((long long)per_sm * sms, nb);
-      k_step_tiles_wp<T, TN, MW * 5 / 6><<<grid, 32 * kWarpsPerBlock, 0, h->stream>>>(pre, post, h->flags, h->nbr27, bv, br,
-                                                                             h->g, om, it, h->n_items, lut);
-      return;
-    }
     if (TH.on)  // the ghost exchange needs 48 registers (fp32)
       k_step_tiles_w<T, TN, MW * 5 / 6, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
           pre, post, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, TH);
@@ -648,6 +637,50 @@ void preload_halo_kernels(const lbm_handle* h) {
 }  // namespace
 
 // -------------------------------------------- pipelined host <-> device copies
+// Pinned staging slots are kept in a small process-wide cache when a handle
+// is destroyed, so the next handle's first upload / readback does not pay
+// cudaHostAlloc (pinning 2 x 64 MB costs tens of ms) -- like the CUDA
+// context, the staging outlives one Simulation.
+static std::mutex g_pin_mu;
+static std::vector<std::pair<void*, size_t>> g_pin_cache;
+
+static void release_pinned(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (g_pin_cache.size() < 4) {
+    g_pin_cache.emplace_back(p, bytes);
+    return;
+  }
+  cudaFreeHost(p);
+}
+
+// both staging slots of h hold at least `bytes`
+static int ensure_pinned(lbm_handle* h, size_t bytes) {
+  if (h->pin_bytes >= bytes && h->pin[0] && h->pin[1]) return 0;
+  for (int b = 0; b < 2; ++b) {
+    release_pinned(h->pin[b], h->pin_bytes);
+    h->pin[b] = nullptr;
+  }
+  h->pin_bytes = bytes;
+  for (int b = 0; b < 2; ++b) {
+    {
+      std::lock_guard<std::mutex> lk(g_pin_mu);
+      for (size_t k = 0; k < g_pin_cache.size(); ++k)
+        if (g_pin_cache[k].second == bytes) {
+          h->pin[b] = g_pin_cache[k].first;
+          g_pin_cache.erase(g_pin_cache.begin() + (long)k);
+          break;
+        }
+    }
+    if (!h->pin[b] && cudaHostAlloc(&h->pin[b], bytes, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      h->pin[b] = nullptr;
+      h->pin_bytes = 0;
+      return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", bytes);
+    }
+  }
+  return 0;
+}
 // host copy split over threads (also spreads the page faults of fresh
 // destination arrays)
 static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
@@ -696,19 +729,7 @@ static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch,
   if (cz > h->g.nz) cz = h->g.nz;
   if (cz > 65535) cz = 65535;
   const size_t slot = (size_t)(cz * pn * bytes_per_node);
-  if (h->pin_bytes < slot) {
-    for (int b = 0; b < 2; ++b) {
-      if (h->pin[b]) cudaFreeHost(h->pin[b]);
-      h->pin[b] = nullptr;
-    }
-    h->pin_bytes = 0;
-    for (int b = 0; b < 2; ++b)
-      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
-      }
-    h->pin_bytes = slot;
-  }
+  if (int rc_ = ensure_pinned(h, slot)) return rc_;
   for (int b = 0; b < 2; ++b)
     if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
   char* dev = nullptr;
@@ -716,6 +737,9 @@ static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch,
   if (e != cudaSuccess) return fail(LBM_ENOMEM, "readback staging: %s", cudaGetErrorString(e));
   const int nz = h->g.nz;
   const int nchunk = (int)((nz + cz - 1) / cz);
+  const char* tv = getenv("LBM_TIMING");
+  const bool timing = tv && tv[0] == '1';
+  double t_wait = 0.0, t_cons = 0.0;
   for (int k = 0; k <= nchunk && e == cudaSuccess; ++k) {
     if (k < nchunk) {
       const int b = k & 1, z0 = (int)(k * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
@@ -728,10 +752,16 @@ static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch,
     }
     if (k > 0 && e == cudaSuccess) {
       const int b = (k - 1) & 1, z0 = (int)((k - 1) * cz), nzc = (int)(nz - z0 < cz ? nz - z0 : cz);
+      const auto w0 = std::chrono::steady_clock::now();
       e = cudaEventSynchronize(h->evc[b]);
+      const auto w1 = std::chrono::steady_clock::now();
       if (e == cudaSuccess) consume(k - 1, z0, nzc, (const char*)h->pin[b]);
+      t_wait += std::chrono::duration<double, std::milli>(w1 - w0).count();
+      t_cons += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w1).count();
     }
   }
+  if (timing) fprintf(stderr, "[lbm timing] readback: %d chunks of %zu B, DMA wait %.3f ms, host copy %.3f ms\n",
+                      nchunk, slot, t_wait, t_cons);
   cudaStreamSynchronize(h->stream);
   cudaFree(dev);
   if (e != cudaSuccess) return fail(LBM_ECUDA, "readback: %s", cudaGetErrorString(e));
@@ -746,19 +776,7 @@ static int pipelined_h2d(lbm_handle* h, void* dev, const void* host, size_t byte
     CK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, h->stream));
     return 0;
   }
-  if (h->pin_bytes < slot) {
-    for (int b = 0; b < 2; ++b) {
-      if (h->pin[b]) cudaFreeHost(h->pin[b]);
-      h->pin[b] = nullptr;
-    }
-    h->pin_bytes = 0;
-    for (int b = 0; b < 2; ++b)
-      if (cudaHostAlloc(&h->pin[b], slot, cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", slot);
-      }
-    h->pin_bytes = slot;
-  }
+  if (int rc_ = ensure_pinned(h, slot)) return rc_;
   for (int b = 0; b < 2; ++b)
     if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
   const size_t n = (bytes + slot - 1) / slot;
@@ -782,19 +800,7 @@ static int pipelined_h2d(lbm_handle* h, void* dev, const void* host, size_t byte
 static int upload_descriptors(lbm_handle* h, uint8_t* dto, uint8_t* dbc, const uint8_t* type, const uint8_t* orient,
                               const int32_t* bc, long long N, int nb, int* err) {
   const size_t half = 32u << 20;  // nodes per chunk: 32 MB of each output per pinned slot
-  if (h->pin_bytes < 2 * half) {
-    for (int b = 0; b < 2; ++b) {
-      if (h->pin[b]) cudaFreeHost(h->pin[b]);
-      h->pin[b] = nullptr;
-    }
-    h->pin_bytes = 0;
-    for (int b = 0; b < 2; ++b)
-      if (cudaHostAlloc(&h->pin[b], 2 * half, cudaHostAllocDefault) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", 2 * half);
-      }
-    h->pin_bytes = 2 * half;
-  }
+  if (int rc_ = ensure_pinned(h, 2 * half)) return rc_;
   for (int b = 0; b < 2; ++b)
     if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
   static const int hw = [] {
@@ -1060,7 +1066,7 @@ void lbm_destroy(lbm_t* h) {
   dev_free(h->sync);
   dev_free(h->herr);
   for (int b = 0; b < 2; ++b) {
-    if (h->pin[b]) cudaFreeHost(h->pin[b]);
+    release_pinned(h->pin[b], h->pin_bytes);
     if (h->evc[b]) cudaEventDestroy(h->evc[b]);
   }
   if (h->ev0) cudaEventDestroy(h->ev0);

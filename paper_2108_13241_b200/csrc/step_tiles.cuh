@@ -386,71 +386,6 @@ k_step_tiles_w(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* 
   if (CUT && cut) tile_ghost_push<T>(f, TH, g, x, y, z);
 }
 
-// Persistent work list (variant 13): each warp walks the items wid, wid + W,
-// ... (W = resident warps of the grid) and loads item k + 1 -- and, once it
-// has arrived, that item's neighbour-table entry, slot-table entry and flag
-// word -- while item k's data loads are in flight, so the metadata chain
-// (item -> table / flags -> data) leaves the critical path of every item but
-// the first.  Same per-node work as k_step_tiles_w.
-template <typename T, int TN, int MINB>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, MINB * 8 / kWarpsPerBlock)
-k_step_tiles_wp(const T* __restrict__ pre, T* __restrict__ post, const uint32_t* __restrict__ flags,
-                const int* __restrict__ nbr27, const T* __restrict__ bcv, const T* __restrict__ bcr, Geo g, T om,
-                const uint4* __restrict__ items, int n_items, const ulonglong2* __restrict__ lut) {
-  const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * kWarpsPerBlock;
-  int wid = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (wid >= n_items) return;  // whole warps
-  WarpItem W = WarpItem::decode<T>(__ldg(items + wid), lane, g);
-  int srel = nbr_rel<T, TN>(nbr27, W.t, lane);
-  ulonglong2 e = __ldg(lut + W.l);
-  uint32_t w = W.uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (W.in ? __ldg(flags + (size_t)W.t * TN + W.l) : 0u);
-#pragma unroll 1
-  for (;;) {
-    const int t = W.t;
-    const bool live = flag_type(w) != SOLID;
-    const bool zfill = sector_needs_zero<T>(live) && g.zero_fill;
-    const T* __restrict__ tb = pre + (size_t)t * (Q * TN);
-    T* __restrict__ tp = post + (size_t)t * (Q * TN);
-    const TileUpLUT up(e);
-    const uint32_t miss = ~w & kMaskBits;
-    T f[Q];
-    f[0] = live ? __ldg(tb + up.p) : (T)0;
-#pragma unroll
-    for (int i = 1; i < Q; ++i) {
-      const int off = __shfl_sync(0xffffffffu, srel, up.code(i)) + up.loc(i);
-      f[i] = live ? __ldg(tb + (((miss >> (opp(i) - 1)) & 1u) ? up.p + opp(i) * TN : off + i * TN)) : (T)0;
-    }
-    // next item's metadata, in flight during this item's collision and stores
-    const int nxt = wid + nw;
-    const bool more = nxt < n_items;
-    WarpItem Wn = W;
-    int srel_n = 0;
-    ulonglong2 en = e;
-    uint32_t wn = 0u;
-    if (more) {
-      Wn = WarpItem::decode<T>(__ldg(items + nxt), lane, g);
-      srel_n = nbr_rel<T, TN>(nbr27, Wn.t, lane);
-      en = __ldg(lut + Wn.l);
-      wn = Wn.uniform ? make_flag(kMaskBits, FLUID, 0, 0) : (Wn.in ? __ldg(flags + (size_t)Wn.t * TN + Wn.l) : 0u);
-    }
-    if (live) {
-      bc_collide<T>(f, w, bcv, bcr, om);
-#pragma unroll
-      for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = f[i];
-    } else if (zfill && W.in) {
-#pragma unroll
-      for (int i = 0; i < Q; ++i) tp[up.p + i * TN] = (T)0;
-    }
-    if (!more) break;
-    wid = nxt;
-    W = Wn;
-    srel = srel_n;
-    e = en;
-    w = wn;
-  }
-}
-
 // A-A z-slabs for tile layouts: like the dense A-A slabs, the neighbour
 // step of a boundary node reads and writes the neighbouring slab's boundary
 // plane directly in ITS tile storage (peer memory; its rank grid row of that
