@@ -675,6 +675,10 @@ static int ensure_pinned(lbm_handle* h, size_t bytes) {
     if (!h->pin[b] && cudaHostAlloc(&h->pin[b], bytes, cudaHostAllocDefault) != cudaSuccess) {
       cudaGetLastError();
       h->pin[b] = nullptr;
+      for (int q = 0; q < 2; ++q) {  // keep the slot that was obtained
+        release_pinned(h->pin[q], bytes);
+        h->pin[q] = nullptr;
+      }
       h->pin_bytes = 0;
       return fail(LBM_ENOMEM, "pinned staging of %zu bytes failed", bytes);
     }
