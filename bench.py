@@ -395,6 +395,8 @@ def main():
         t_step = time.perf_counter()
         fields = s2.density_field() if big else s2.macroscopic_fields()
         t1 = time.perf_counter()
+        if os.environ.get("LBM_TIMING") == "1":
+            sys.stderr.write(f"[bench timing] e2e readback call {1e3 * (t1 - t_step):.3f} ms\n")
         e2e = {"value": nons * args.steps / (t1 - t0) / 1e6, "unit": "MLUPS",
                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                "what": "Simulation(geometry) [descriptor upload] + initialize + step(K) + "

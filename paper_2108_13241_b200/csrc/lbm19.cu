@@ -191,6 +191,41 @@ void dev_free(void* p) {
   if (p) cudaFree(p);
 }
 
+// Setup temporaries and readback staging come from the stream-ordered pool
+// (cudaMallocAsync / cudaFreeAsync on the solver stream): no device-wide
+// synchronisation per free, and the pool keeps the memory for the next
+// handle -- after a large cudaFree, plain cudaMalloc / cudaFree of these
+// buffers measured 20-600 ms (profiles/setup_phases_r02*.txt).
+template <typename P>
+int tmp_alloc(lbm_handle* h, P** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMallocAsync(&q, bytes ? bytes : 16, h->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? LBM_ENOMEM : LBM_ECUDA, "cudaMallocAsync(%zu bytes): %s", bytes,
+                cudaGetErrorString(e));
+  }
+  *p = (P*)q;
+  return 0;
+}
+
+void tmp_free(const lbm_handle* h, void* p) {
+  if (p) cudaFreeAsync(p, h->stream);
+}
+
+// keep freed pool memory cached for the next temporaries (once per device)
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long keep = 4ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
 // Copies of state the solver stream touches go through that stream: the
 // legacy default stream does not order against a non-blocking stream, and a
 // pageable cudaMemcpy can return before its DMA has landed.
@@ -715,6 +750,11 @@ static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, 
 // at a time; asking for transparent huge pages first turns the readback's
 // fault-in into 2 MB faults (no-op where THP is off).
 static void advise_huge(void* p, size_t bytes) {
+  static const bool off = [] {
+    const char* v = getenv("LBM_THP");
+    return v && v[0] == '0';
+  }();
+  if (off) return;
   const uintptr_t a = ((uintptr_t)p + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
   const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((2u << 20) - 1);
   if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
@@ -733,11 +773,14 @@ static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch,
   if (cz > h->g.nz) cz = h->g.nz;
   if (cz > 65535) cz = 65535;
   const size_t slot = (size_t)(cz * pn * bytes_per_node);
+  const auto s0 = std::chrono::steady_clock::now();
   if (int rc_ = ensure_pinned(h, slot)) return rc_;
   for (int b = 0; b < 2; ++b)
     if (!h->evc[b]) CK(cudaEventCreateWithFlags(&h->evc[b], cudaEventDisableTiming));
+  keep_pool(h->d.device);
   char* dev = nullptr;
-  cudaError_t e = cudaMalloc(&dev, 2 * slot);
+  cudaError_t e = cudaMallocAsync((void**)&dev, 2 * slot, h->stream);
+  const auto s1 = std::chrono::steady_clock::now();
   if (e != cudaSuccess) return fail(LBM_ENOMEM, "readback staging: %s", cudaGetErrorString(e));
   const int nz = h->g.nz;
   const int nchunk = (int)((nz + cz - 1) / cz);
@@ -764,10 +807,17 @@ static int pipelined_d2h(lbm_handle* h, long long bytes_per_node, Launch launch,
       t_cons += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w1).count();
     }
   }
-  if (timing) fprintf(stderr, "[lbm timing] readback: %d chunks of %zu B, DMA wait %.3f ms, host copy %.3f ms\n",
-                      nchunk, slot, t_wait, t_cons);
+  const auto s2 = std::chrono::steady_clock::now();
+  cudaFreeAsync(dev, h->stream);
   cudaStreamSynchronize(h->stream);
-  cudaFree(dev);
+  if (timing) {
+    const auto s3 = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr,
+            "[lbm timing] readback: staging %.3f ms, %d chunks of %zu B (DMA wait %.3f ms, host copy %.3f ms), "
+            "loop %.3f ms, teardown %.3f ms\n",
+            ms(s0, s1), nchunk, slot, t_wait, t_cons, ms(s1, s2), ms(s2, s3));
+  }
   if (e != cudaSuccess) return fail(LBM_ECUDA, "readback: %s", cudaGetErrorString(e));
   return 0;
 }
@@ -1124,7 +1174,8 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
   const int nbt = nb > 0 ? nb : 1;
   PhaseTimer pt(h->stream);
   // temporaries
-  if ((rc = dev_alloc(h, &dtype_, N)) || (rc = dev_alloc(h, &dbc, N)) || (rc = dev_alloc(h, &derr, 16)))
+  keep_pool(h->d.device);
+  if ((rc = tmp_alloc(h, &dtype_, N)) || (rc = tmp_alloc(h, &dbc, N)) || (rc = tmp_alloc(h, &derr, 16)))
     goto done;
   pt.mark("alloc temporaries");
   if ((rc = upload_descriptors(h, dtype_, dbc, type, orient, bc_index, N, nb, &herr_host))) goto done;
@@ -1136,13 +1187,13 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
   h->has_glo = ghost_lo != nullptr;  // z-slab: links cross z = -1 / z = nz into a neighbour
   h->has_ghi = ghost_hi != nullptr;
   if (ghost_lo) {
-    if ((rc = dev_alloc(h, &dglo, plane_nodes))) goto done;
+    if ((rc = tmp_alloc(h, &dglo, plane_nodes))) goto done;
     CK(cudaMemcpyAsync(dglo, ghost_lo, plane_nodes, cudaMemcpyHostToDevice, h->stream));
   } else if (g.pzw) {
     dglo = nullptr;  // wrap handled below
   }
   if (ghost_hi) {
-    if ((rc = dev_alloc(h, &dghi, plane_nodes))) goto done;
+    if ((rc = tmp_alloc(h, &dghi, plane_nodes))) goto done;
     CK(cudaMemcpyAsync(dghi, ghost_hi, plane_nodes, cudaMemcpyHostToDevice, h->stream));
   }
   {
@@ -1199,8 +1250,8 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       }
     } else {
       const long long G = h->ntiles_grid;
-      if ((rc = dev_alloc(h, &h->rank, G * 4)) || (rc = dev_alloc(h, &keep, G * 4)) ||
-          (rc = dev_alloc(h, &scan, G * 4)))
+      if ((rc = dev_alloc(h, &h->rank, G * 4)) || (rc = tmp_alloc(h, &keep, G * 4)) ||
+          (rc = tmp_alloc(h, &scan, G * 4)))
         goto done;
       const int keep_all = h->d.layout == LBM_LAYOUT_TILE;
       pt.mark("upload descriptors");
@@ -1209,7 +1260,7 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
       size_t tmp_bytes = 0;
       if (G > 0x7fffffffLL) { rc = fail(LBM_EINVAL, "too many tiles"); goto done; }
       CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, keep, scan, (int)G, h->stream));
-      if ((rc = dev_alloc(h, (char**)&cub_tmp, tmp_bytes))) goto done;
+      if ((rc = tmp_alloc(h, (char**)&cub_tmp, tmp_bytes))) goto done;
       CK(cub::DeviceScan::ExclusiveSum(cub_tmp, tmp_bytes, keep, scan, (int)G, h->stream));
       int last_scan = 0, last_keep = 0;
       CK(cudaMemcpyAsync(&last_scan, scan + G - 1, 4, cudaMemcpyDeviceToHost, h->stream));
@@ -1375,12 +1426,23 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
     // (a 2^31-node domain needs every byte: 163 GB AA PDFs + 8.6 GB flags)
     for (void** p : {(void**)&dtype_, (void**)&dorient, (void**)&dbc, (void**)&dglo, (void**)&dghi,
                      (void**)&keep, (void**)&scan, (void**)&cub_tmp}) {
-      dev_free(*p);
+      tmp_free(h, *p);
       *p = nullptr;
     }
     pt.mark("geometry done");
     // PDF buffers
     const size_t fbytes = (size_t)(buf_elems(h) > 0 ? buf_elems(h) : 64) * h->esize;
+    {
+      // a domain that fills HBM needs the pool's cached temporaries back
+      size_t fr = 0, tot = 0;
+      CK(cudaStreamSynchronize(h->stream));
+      cudaMemGetInfo(&fr, &tot);
+      if (fr < (g.aa ? 1 : 2) * fbytes + (1ull << 30)) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, h->d.device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        cudaGetLastError();
+      }
+    }
     if ((rc = dev_alloc(h, (char**)&h->f[0], fbytes))) goto done;
     if (!g.aa && (rc = dev_alloc(h, (char**)&h->f[1], fbytes))) goto done;  // AA: one buffer
     CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->stream));
@@ -1394,15 +1456,15 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
 done:
   {
     cudaStreamSynchronize(h->stream);
-    dev_free(dtype_);
-    dev_free(dorient);
-    dev_free(dbc);
-    dev_free(dglo);
-    dev_free(dghi);
-    dev_free(derr);
-    dev_free(keep);
-    dev_free(scan);
-    dev_free(cub_tmp);
+    tmp_free(h, dtype_);
+    tmp_free(h, dorient);
+    tmp_free(h, dbc);
+    tmp_free(h, dglo);
+    tmp_free(h, dghi);
+    tmp_free(h, derr);
+    tmp_free(h, keep);
+    tmp_free(h, scan);
+    tmp_free(h, cub_tmp);
     // recompute resident bytes (temporaries released)
     if (h->geometry) {
       long long b = (h->g.aa ? 1LL : 2LL) * (buf_elems(h) > 0 ? buf_elems(h) : 64) * h->esize + h->nflags * 4;
