@@ -384,7 +384,27 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
   const unsigned fi = ((unsigned)z * g.ny + y) * g.nxp + x;
   const unsigned s = fi + (unsigned)g.plane;
   const uint32_t ub = __ldg(ubits + (fi >> 10));
-  const uint32_t w = ((ub >> ((fi >> 5) & 31)) & 1u) ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
+  const bool uni = (ub >> ((fi >> 5) & 31)) & 1u;  // warp-uniform: one chunk = one warp
+  if (NB && uni && !((z == 0 && H.lo[0]) || (z == g.nz - 1 && H.hi[0]))) {
+    // uniform chunk (all FLUID / wall, full masks) off the slab cut: every
+    // link present, no closure -- the arithmetic of the general path below
+    // without its selects and fix-ups
+    const UpOffsets o(g, x, y, z);
+    T f[Q];
+    f[0] = LDA(P.f[0] + s);
+#pragma unroll
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));
+    T rho, vx, vy, vz;
+    moments19(f, rho, vx, vy, vz);
+    collide19(f, rho, vx, vy, vz, om);
+    const unsigned s2 = opaque(s);
+    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
+    P.f[0][s2] = f[0];
+#pragma unroll
+    for (int i = 1; i < Q; ++i) P.f[i][o2.up(s2, opp(i))] = f[i];
+    return;
+  }
+  const uint32_t w = uni ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
   // no zero-fill of solid lanes here (unlike the AB kernel): every sector
   // this step writes was read by the same step, so it sits in L2 whole and a
   // partial store needs no DRAM read-for-merge; zero stores from solid lanes
