@@ -91,10 +91,12 @@ def measure_device(lb, workload, geom, params, layout, scheme, tile, dtype, rho0
     sim = lb.Simulation(geom, params, layout=layout, scalar=scalar, device=device, scheme=scheme,
                         tile=tile)
     sim.initialize(rho0)
-    sim.step(warmup)
-    launches0 = sim.launches_total
     with ClockSampler(device) as clk:
+        sim.step(warmup)
+        launches0 = sim.launches_total
+        clk.mark_start()
         sim.step(steps)    # CUDA events on the solver stream around K launches
+        clk.mark_end()
     ms = sim.last_step_ms
     launches = sim.launches_total - launches0
     clocks = clk.summary()
@@ -170,9 +172,15 @@ def build_workload(name, rank=0, world=1):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    The sampler starts before the warm-up (nvidia-smi needs ~0.1 s to produce
+    its first row); mark_start() / mark_end() bracket the timed region and
+    summary() keeps the rows stamped inside it -- or, for a region shorter
+    than the 20 ms sampling interval, the rows nearest to it (within 0.1 s),
+    and says so."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -180,6 +188,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -187,11 +196,17 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -202,16 +217,30 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        import datetime
         rows = []
         try:
             with open(self.path) as fh:
                 for line in fh:
                     parts = [p.strip() for p in line.split(",")]
-                    if len(parts) >= 9:
-                        rows.append(parts)
+                    if len(parts) >= 10:
+                        try:
+                            ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                        except ValueError:
+                            ts = None
+                        rows.append((ts, parts[1:]))
             os.unlink(self.path)
         except Exception:
             pass
+        window = "whole sampler run"
+        if self.t0 is not None and self.t1 is not None and rows:
+            inside = [r for r in rows if r[0] is not None and self.t0 <= r[0] <= self.t1]
+            if inside:
+                rows, window = inside, "inside the timed region"
+            else:
+                near = [r for r in rows if r[0] is not None and self.t0 - 0.1 <= r[0] <= self.t1 + 0.1]
+                rows, window = near, "within 0.1 s of a timed region shorter than the sampling interval"
+        rows = [r[1] for r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
@@ -220,7 +249,7 @@ class ClockSampler:
         reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "window": window}
 
 
 CPU_SLAB_NZ = 32   # the CPU sample: 512 x 512 x 32 z-periodic slab of C2

@@ -74,9 +74,11 @@ def run_multi(args, rank, world, local):
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.mark_start()
         t0 = time.perf_counter()
         sim.step(args.steps)
         t1 = time.perf_counter()
+        clk.mark_end()
     dist.barrier()
     ms = sim.last_step_ms
     t = torch.tensor([ms, t1 - t0], dtype=torch.float64, device=dev)
