@@ -179,16 +179,23 @@ int lbm_get_flags(lbm_t* h, uint32_t* out);
 int lbm_get_tile_index(lbm_t* h, int32_t* tiles, int32_t* nbr27, int64_t* n_tiles);
 int lbm_get_stats(lbm_t* h, lbm_stats* out);
 
-/* z-slab halo exchange (multi-GPU, dense layouts).  Each slab handle covers
- * global planes [z0, z0 + nz); after every step the outgoing populations of
- * its two boundary planes are stored by the step kernel itself straight into
- * the neighbouring slab's ghost plane (peer memory: same process = device
- * pointers + peer access, other process = CUDA IPC), and device-side flags
- * order the steps (no host round trip).  lbm_halo_export writes an opaque
+/* z-slab halo exchange (multi-GPU; dense and tile layouts, AB and A-A).
+ * Each slab handle covers global planes [z0, z0 + nz); during every step the
+ * outgoing populations of its two boundary planes are stored by the step
+ * kernel itself straight into the neighbouring slab's ghost plane (A-A: into
+ * the neighbour's boundary plane) through peer memory (same process = device
+ * pointers + peer access, other process = CUDA IPC).  Device-side epochs
+ * order the steps (no host round trip; the boundary planes run first and
+ * signal, the interior overlaps the neighbours' next step; 32-step sequences
+ * replay from CUDA graphs).  lbm_halo_export writes an opaque
  * LBM_HALO_BLOB_BYTES blob the caller ships to the neighbours (e.g. with
  * torch.distributed.all_gather_object); lbm_halo_connect opens the lower and
  * upper neighbour's blob (NULL = no neighbour on that side).  All slabs must
- * then make the same sequence of init / step calls. */
+ * then make the same sequence of init / step / state-write calls (a state
+ * write on one slab alone leaves the epochs out of step: the next wait times
+ * out with LBM_ENCCL).  A handle whose geometry has a ghost plane refuses to
+ * step until that side is connected, and refuses lbm_set_geometry while
+ * connected. */
 #define LBM_HALO_BLOB_BYTES 512
 int lbm_halo_export(lbm_t* h, void* blob, size_t* bytes);
 int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob);

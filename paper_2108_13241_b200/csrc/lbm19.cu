@@ -486,10 +486,19 @@ void launch_tiles_aa(lbm_handle* h, T* F) {
     // 48 resident warps for both phases (40 registers; the neighbour step
     // spills 8 B and still measured 0-1 % faster than 40 warps at 48
     // registers, profiles/ab_aa_warp_list_r01.txt)
-    if (h->parity == 0 && halo_on(h))  // z-slab: the cut's links reach into the neighbours
-      k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 2, true><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
-          F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut, make_tile_aa_halo<T>(h));
-    else if (h->parity == 0)
+    if (h->parity == 0 && halo_on(h)) {
+      // z-slab: the boundary tile planes' items (ordered first) reach into the
+      // neighbours; the interior items run the plain neighbour step
+      const int nbi = h->n_items_b, nin = h->n_items - h->n_items_b;
+      if (nbi > 0)
+        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 5 : 2, true>
+            <<<(unsigned)((nbi + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
+                F, h->flags, h->nbr27, bv, br, h->g, om, it, nbi, lut, make_tile_aa_halo<T>(h));
+      if (nin > 0)
+        k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3>
+            <<<(unsigned)((nin + kWarpsPerBlock - 1) / kWarpsPerBlock), 32 * kWarpsPerBlock, 0, h->stream>>>(
+                F, h->flags, h->nbr27, bv, br, h->g, om, it + nbi, nin, lut);
+    } else if (h->parity == 0)
       k_step_tiles_aa_w<T, TN, 1, sizeof(T) == 4 ? 6 : 3><<<nb, 32 * kWarpsPerBlock, 0, h->stream>>>(
           F, h->flags, h->nbr27, bv, br, h->g, om, it, h->n_items, lut);
     else
