@@ -210,6 +210,16 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # a region shorter than nvidia-smi's start-up: wait (<= 0.5 s) for
+            # the first row, taken while the clocks are still at their load value
+            t_end = time.time() + 0.5
+            while time.time() < t_end:
+                try:
+                    if os.path.getsize(self.path) > 0:
+                        break
+                except OSError:
+                    break
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -239,7 +249,12 @@ class ClockSampler:
                 rows, window = inside, "inside the timed region"
             else:
                 near = [r for r in rows if r[0] is not None and self.t0 - 0.1 <= r[0] <= self.t1 + 0.1]
-                rows, window = near, "within 0.1 s of a timed region shorter than the sampling interval"
+                if near:
+                    rows, window = near, "within 0.1 s of a timed region shorter than the sampling interval"
+                else:
+                    after = [r for r in rows if r[0] is not None and self.t1 < r[0] <= self.t1 + 0.5][:1]
+                    rows, window = after, ("first row after a timed region shorter than nvidia-smi's start-up "
+                                           "(within 0.5 s)")
         rows = [r[1] for r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
