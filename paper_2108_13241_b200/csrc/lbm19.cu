@@ -1540,6 +1540,36 @@ int lbm_set_omega(lbm_t* h, double omega) {
   return 0;
 }
 
+// kGraphSteps steps starting at parity p0, captured into h->graph[p0] once
+static int capture_graph(lbm_handle* h, int p0) {
+  cudaGraphExec_t& ge = h->graph[p0];
+  if (ge) return 0;
+  const bool halo = halo_on(h);
+  const int keep = h->parity;
+  const long long l0 = h->launches;
+  h->parity = p0;
+  cudaGraph_t gr = nullptr;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < kGraphSteps; ++k) {
+    void* post = h->g.aa ? h->f[0] : h->f[1 - h->parity];
+    if (h->esize == 4) {
+      if (halo) slab_step<float>(h, pre_buf(h), post); else launch_step<float>(h, pre_buf(h), post);
+    } else {
+      if (halo) slab_step<double>(h, pre_buf(h), post); else launch_step<double>(h, pre_buf(h), post);
+    }
+    h->parity ^= 1;
+  }
+  CK(cudaStreamEndCapture(h->stream, &gr));
+  h->parity = keep;
+  h->graph_launches = h->launches - l0;
+  h->launches = l0;
+  cudaError_t e = cudaGraphInstantiate(&ge, gr, 0);
+  cudaGraphDestroy(gr);
+  if (e == cudaSuccess) e = cudaGraphUpload(ge, h->stream);
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "cuda graph: %s", cudaGetErrorString(e));
+  return 0;
+}
+
 int lbm_step_async(lbm_t* h, int64_t n) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   NvtxRange nv("lbm_step");
@@ -1563,31 +1593,10 @@ int lbm_step_async(lbm_t* h, int64_t n) {
   // launch-bound small domains: replay a captured CUDA graph of kGraphSteps
   // steps (an even count, so it starts and ends on the same parity)
   // z-slabs capture their wait / boundary / signal / interior sequence too
-  // (the epochs live on the device)
+  // (the epochs live on the device; connected slabs capture at connect time)
   if (h->use_graph && n >= kGraphSteps) {
+    if (int rc = capture_graph(h, h->parity)) return rc;
     cudaGraphExec_t& ge = h->graph[h->parity];
-    const long long l0 = h->launches;
-    if (!ge) {
-      cudaGraph_t gr = nullptr;
-      const int p0 = h->parity;
-      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-      for (int k = 0; k < kGraphSteps; ++k) {
-        void* post = h->g.aa ? h->f[0] : h->f[1 - h->parity];
-        if (h->esize == 4) {
-          if (halo) slab_step<float>(h, pre_buf(h), post); else launch_step<float>(h, pre_buf(h), post);
-        } else {
-          if (halo) slab_step<double>(h, pre_buf(h), post); else launch_step<double>(h, pre_buf(h), post);
-        }
-        h->parity ^= 1;
-      }
-      CK(cudaStreamEndCapture(h->stream, &gr));
-      h->parity = p0;
-      h->graph_launches = h->launches - l0;
-      h->launches = l0;
-      cudaError_t e = cudaGraphInstantiate(&ge, gr, 0);
-      cudaGraphDestroy(gr);
-      if (e != cudaSuccess) return fail(LBM_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
-    }
     while (n >= kGraphSteps) {
       CK(cudaGraphLaunch(ge, h->stream));
       h->launches += h->graph_launches;
@@ -2124,6 +2133,14 @@ int lbm_halo_connect(lbm_t* h, const void* lo_blob, const void* hi_blob) {
   }
   if (h->esize == 4) preload_halo_kernels<float>(h); else preload_halo_kernels<double>(h);
   drop_graphs(h);  // captured step sequences change with the neighbours
+  // capture and upload both parities' step graphs now, while no slab of this
+  // process spins on a halo wait: instantiating them later, between launches
+  // of neighbouring slabs driven from the same host thread, could wait behind
+  // those spinning kernels
+  if (h->use_graph && (h->lo.on || h->hi.on)) {
+    if ((rc = capture_graph(h, 0)) || (rc = capture_graph(h, 1))) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+  }
   h->halo_dirty = true;
   return 0;
 }
