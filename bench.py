@@ -351,6 +351,8 @@ def main():
     ap.add_argument("--tile", default="4,8,16",
                     help="tile edges x,y,z for tile layouts (4x8x16: measured best of 7 shapes, "
                          "profiles/sparse_r01.md; the API default is 8x8x8)")
+    ap.add_argument("--layout", default=None, choices=["dense", "tile", "pointer_tile", "bitmask_node"],
+                    help="override the workload's storage layout (design experiments)")
     ap.add_argument("--scheme", default=None, choices=["ab", "aa"],
                     help="PDF storage: two buffers (ab) or one in place (aa)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -385,6 +387,7 @@ def main():
         except Exception as exc:  # reported, never fatal for the GPU number
             cpu = {"value": None, "error": repr(exc)}
     geom, params, layout, desc, rho0 = build_workload(workload)
+    layout = args.layout or layout
     scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
     tile = tuple(int(v) for v in args.tile.split(","))
     scalar = np.float32 if args.dtype == "f32" else np.float64
