@@ -39,7 +39,6 @@
 #include <sys/mman.h>
 #include <string>
 #include <thread>
-#include <sys/mman.h>
 #include <vector>
 
 #include "d3q19.cuh"
