@@ -348,9 +348,9 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
                     help="storage/arithmetic type (the reference's Simulation defaults to float64)")
-    ap.add_argument("--tile", default="4,8,16",
-                    help="tile edges x,y,z for tile layouts (4x8x16: measured best of 7 shapes, "
-                         "profiles/sparse_r01.md; the API default is 8x8x8)")
+    ap.add_argument("--tile", default="4,4,8",
+                    help="tile edges x,y,z for tile layouts (4x4x8, the API default: measured best or level "
+                         "across porosity and C4 with the work list, profiles/tile_sweep_r02ag.txt)")
     ap.add_argument("--layout", default=None, choices=["dense", "tile", "pointer_tile", "bitmask_node"],
                     help="override the workload's storage layout (design experiments)")
     ap.add_argument("--scheme", default=None, choices=["ab", "aa"],

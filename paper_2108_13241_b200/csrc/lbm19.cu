@@ -1369,11 +1369,13 @@ int lbm_set_geometry(lbm_t* h, const uint8_t* type, const uint8_t* orient, const
           if ((rc = dev_alloc(h, &h->items, (it.size() ? it.size() : 4) * 4))) goto done;
           if (!it.empty()) CK(scopy(h, h->items, it.data(), it.size() * 4, cudaMemcpyHostToDevice));
         }
-        // tiles with mean live-brick fraction < 0.85 (porosity up to ~0.7, tube
-        // networks) run the warp work list by default: measured +1-9 % over the
-        // CTA-per-tile kernels there, -3 % on fuller tiles (profiles/sparse_r01.md)
+        // the warp work list is the default for every tile shape unless the
+        // kept tiles are (almost) all live bricks: round 2 measured it ahead
+        // of or level with one CTA per tile at every porosity and tile shape
+        // (profiles/tile_sweep_r02ag.txt; round 1 had enabled it only for
+        // 512-node tiles below live fraction 0.85)
         const double live_frac = T > 0 ? (double)live / ((double)T * (g.tn / bn)) : 1.0;
-        h->auto_wlist = h->wlist_ok && h->d.layout == LBM_LAYOUT_POINTER_TILE && g.tn == 512 && live_frac < 0.85;
+        h->auto_wlist = h->wlist_ok && live_frac < 0.99;
         h->live_frac = live_frac;
         // per tile: nbr27 + brick masks; per live, non-uniform brick: its flag
         // words; the work list when it is used

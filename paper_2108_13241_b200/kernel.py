@@ -274,7 +274,7 @@ class Simulation:
     (reference kernel.py:155-311)."""
 
     def __init__(self, geometry, params, layout=LayoutKind.DENSE, scalar=np.float64,
-                 device=0, tile=(8, 8, 8), slab=None, scheme="ab"):
+                 device=0, tile=(4, 4, 8), slab=None, scheme="ab"):
         self.geometry = geometry
         self.params = params
         self.layout = LayoutKind.parse(layout)

@@ -1,7 +1,7 @@
 """Parity at the BASELINE configs' full sizes (BASELINE.json configs C2-C4).
 
 * C2 dense channel 512^3 and C3 random-sphere porous 512^3 (phi ~0.5 and
-  ~0.1, pointer_tile 4x8x16 tiles, the default warp work-list kernel): the
+  ~0.1, pointer_tile with the default 4x4x8 tiles and warp work-list kernel): the
   GPU state after 5 steps (both A-A storage phases covered: 5 is odd) equals
   the Numba oracle's bitwise, f_i on every node and direction -- the
   reference's mixed-BC oracle agreement test (pkg/tests/test_kernel.py:
@@ -25,7 +25,8 @@ import paper_2108_13241_b200 as lb
 pytestmark = pytest.mark.gpu
 
 STEPS = 5
-TILE = (4, 8, 16)
+TILE = (4, 4, 8)        # the default tile shape
+TILE_C4 = (4, 8, 16)    # C4: a tile buffer above 2^31 elements
 
 
 def _oracle(geom, omega, rho0, steps):
@@ -82,9 +83,10 @@ def test_c4_vascular1024_tiles_equal_dense_aa():
         sims["dense_aa"] = lb.Simulation(geom, params, layout="dense", scalar=np.float32, scheme="aa")
         for scheme in ("ab", "aa"):
             sims[f"tile_{scheme}"] = lb.Simulation(geom, params, layout="pointer_tile",
-                                                   scalar=np.float32, scheme=scheme, tile=TILE)
+                                                   scalar=np.float32, scheme=scheme, tile=TILE_C4)
         st = sims["tile_ab"].stats()
         assert st.n_tiles * 19 * 512 > 2 ** 31, "the tile buffer must exceed 2^31 elements"
+        sims["tile_ab_default"] = lb.Simulation(geom, params, layout="pointer_tile", scalar=np.float32, tile=TILE)
         for s in sims.values():
             s.initialize(1.0)
         for steps in (STEPS, 1):   # odd then even step count: both A-A phases
@@ -92,7 +94,7 @@ def test_c4_vascular1024_tiles_equal_dense_aa():
                 s.step(steps)
             for z0 in range(0, 1024, 128):
                 base = sims["dense_aa"].macroscopic_box(z=(z0, z0 + 128))
-                for name in ("tile_ab", "tile_aa"):
+                for name in ("tile_ab", "tile_aa", "tile_ab_default"):
                     got = sims[name].macroscopic_box(z=(z0, z0 + 128))
                     for a, b in zip(got, base):
                         assert np.array_equal(a, b), (name, z0)
@@ -100,6 +102,7 @@ def test_c4_vascular1024_tiles_equal_dense_aa():
             masses = [s.total_mass() for s in sims.values()]
             assert masses[1] == pytest.approx(masses[0], rel=1e-9)
             assert masses[2] == pytest.approx(masses[0], rel=1e-9)
+            assert masses[3] == pytest.approx(masses[0], rel=1e-9)
     finally:
         for s in sims.values():
             s.close()

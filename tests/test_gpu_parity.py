@@ -457,23 +457,25 @@ def test_boundary_table_limit_and_bad_descriptors():
         lb.Simulation(g2, params_for(1.1), scalar=np.float32)
 
 
-@pytest.mark.parametrize("phi", [0.15, 0.5, 0.95])
+@pytest.mark.parametrize("phi", [0.15, 0.5, 0.95, 1.0])
 def test_default_tile_kernel_choice_is_bitwise(phi):
     """The tile kernel is picked from the live-brick fraction of the kept
-    tiles (warp work list + select below 0.85, speculative CTA per tile
-    above); every choice reproduces the oracle bitwise."""
+    tiles (warp work list + select below 0.99, speculative CTA per tile for
+    (almost) fully live tiles); every choice reproduces the oracle bitwise."""
     from oracle.step19 import OracleSim
     geom = lb.build_porous_random(64, phi, seed=2, radius_range=(3, 9), dims=(64, 48, 32))
     params = lb.FlowParams.from_viscosity(U=0.05, L=47, nu=0.2)
-    sim = lb.Simulation(geom, params, layout="pointer_tile", scalar=np.float32)
-    # live-brick fraction of the kept 8^3 tiles (2x2x2 bricks), as the library computes it
+    sim = lb.Simulation(geom, params, layout="pointer_tile", scalar=np.float32)   # the default tile
+    # live-brick fraction of the kept tiles (2x2x2 bricks), as the library computes it
+    ex, ey, ez = sim.tile
     ns = geom.descriptors.type_tag != lb.NodeType.SOLID
     nz, ny, nx = ns.shape
     b = ns.reshape(nz // 2, 2, ny // 2, 2, nx // 2, 2).any(axis=(1, 3, 5))
-    bt = b.reshape(nz // 8, 4, ny // 8, 4, nx // 8, 4).sum(axis=(1, 3, 5))
+    bx, by, bz = ex // 2, ey // 2, ez // 2
+    bt = b.reshape(nz // ez, bz, ny // ey, by, nx // ex, bx).sum(axis=(1, 3, 5))
     kept = bt > 0
-    live_frac = bt[kept].sum() / (kept.sum() * 64)
-    assert bool(sim.stats().tile_work_list) == (live_frac < 0.85)
+    live_frac = bt[kept].sum() / (kept.sum() * bx * by * bz)
+    assert bool(sim.stats().tile_work_list) == (live_frac < 0.99)
     sim.initialize(1.004)
     sim.step(9)
     d = geom.descriptors
