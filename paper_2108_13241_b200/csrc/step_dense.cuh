@@ -389,34 +389,19 @@ __global__ void __launch_bounds__(128, MINB) k_step_dense_aa(const Planes1<T> P,
     // uniform chunk (all FLUID / wall, full masks) off the slab cut: every
     // link present, no closure -- the arithmetic of the general path below
     // without its selects and fix-ups
+    const UpOffsets o(g, x, y, z);
     T f[Q];
     f[0] = LDA(P.f[0] + s);
-    // away from the domain edges (and periodic wraps) every offset is a
-    // constant multiple of the row / plane pitch (unsigned wrap arithmetic)
-    const bool inner = x > 0 && x < g.nx - 1 && y > 0 && y < g.ny - 1 && !(g.pzw && (z == 0 || z == g.nz - 1));
-    const unsigned py = (unsigned)g.nxp, pz = (unsigned)g.plane;
-    auto step = [&](int i) { return (unsigned)cx(i) + (unsigned)cy(i) * py + (unsigned)cz(i) * pz; };  // slot of x + c_i - x
-    if (inner) {
 #pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + (s - step(i)));
-    } else {
-      const UpOffsets o(g, x, y, z);
-#pragma unroll
-      for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));
-    }
+    for (int i = 1; i < Q; ++i) f[i] = LDA(P.f[opp(i)] + o.up(s, i));
     T rho, vx, vy, vz;
     moments19(f, rho, vx, vy, vz);
     collide19(f, rho, vx, vy, vz, om);
     const unsigned s2 = opaque(s);
+    const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
     P.f[0][s2] = f[0];
-    if (inner) {
 #pragma unroll
-      for (int i = 1; i < Q; ++i) P.f[i][s2 + step(i)] = f[i];
-    } else {
-      const UpOffsets o2(g, opaque(x), opaque(y), opaque(z));
-#pragma unroll
-      for (int i = 1; i < Q; ++i) P.f[i][o2.up(s2, opp(i))] = f[i];
-    }
+    for (int i = 1; i < Q; ++i) P.f[i][o2.up(s2, opp(i))] = f[i];
     return;
   }
   const uint32_t w = uni ? make_flag(kMaskBits, FLUID, 0, 0) : __ldg(flags + fi);
