@@ -114,6 +114,7 @@ def measure_device(lb, workload, geom, params, layout, scheme, tile, dtype, rho0
     sane = bool(np.isfinite(sim.total_mass()))
     tiled = layout in ("tile", "pointer_tile")
     kern = expected_kernel(layout, scheme, dtype, bool(st.tile_work_list))
+    tile = sim.tile if tiled else None     # the facade's choice when tile is None
     sim.close()
     del sim
     return {"value": mlups, "unit": "MLUPS", "mlups": mlups, "frac": achieved / peak, "steps": steps,
@@ -123,7 +124,8 @@ def measure_device(lb, workload, geom, params, layout, scheme, tile, dtype, rho0
             "porosity": nons / float(st.n_nodes), "stats": st, "launches": launches,
             "gpu_launches": int(launches), "clocks": clocks, "finite": sane, "kernel": kern,
             "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile") if tiled else None),
-            "traffic": ncu_traffic(workload, dtype, scheme, tile if tiled else None, kern)}
+            "tile": list(tile) if tiled else None,
+            "traffic": ncu_traffic(workload, dtype, scheme, tile, kern)}
 
 
 def build_workload(name, rank=0, world=1):
@@ -348,9 +350,10 @@ def main():
     ap.add_argument("--workload", default=None)
     ap.add_argument("--dtype", default="f32", choices=["f32", "f64"],
                     help="storage/arithmetic type (the reference's Simulation defaults to float64)")
-    ap.add_argument("--tile", default="4,4,8",
-                    help="tile edges x,y,z for tile layouts (4x4x8, the API default: measured best or level "
-                         "across porosity and C4 with the work list, profiles/tile_sweep_r02ag.txt)")
+    ap.add_argument("--tile", default="auto",
+                    help="tile edges x,y,z for tile layouts, or 'auto' (the API default: 4x4x8, or 4x4x4 "
+                         "when the kept 4x4x8 tiles are < 70 %% non-solid; profiles/tile_sweep_r02ag.txt, "
+                         "profiles/ab_tile_fill_r02al.txt)")
     ap.add_argument("--layout", default=None, choices=["dense", "tile", "pointer_tile", "bitmask_node"],
                     help="override the workload's storage layout (design experiments)")
     ap.add_argument("--scheme", default=None, choices=["ab", "aa"],
@@ -389,7 +392,7 @@ def main():
     geom, params, layout, desc, rho0 = build_workload(workload)
     layout = args.layout or layout
     scheme = args.scheme or ("aa" if workload == "c5" else DEFAULT_SCHEME)
-    tile = tuple(int(v) for v in args.tile.split(","))
+    tile = None if args.tile == "auto" else tuple(int(v) for v in args.tile.split(","))
     scalar = np.float32 if args.dtype == "f32" else np.float64
     esz = np.dtype(scalar).itemsize
     if args.variants:
@@ -412,7 +415,7 @@ def main():
             peak, _ = measured_peak()
             alg = nons * 2 * 19 * esz + int(sim.stats().meta_bytes_per_step)
             frac = alg / (ms / args.steps / 1e3) / 1e9 / peak
-            print(json.dumps({"workload": workload, "variant": v, "tile": args.tile, "mlups": round(mlups),
+            print(json.dumps({"workload": workload, "variant": v, "tile": list(sim.tile), "mlups": round(mlups),
                               "frac": round(frac, 4), "alg_B_per_node": round(alg / nons, 2),
                               "ms_per_step": ms / args.steps}), flush=True)
             sim.close()
@@ -479,7 +482,7 @@ def main():
                                    max(args.steps, 500), args.warmup)
                 sparse[w] = {k: m[k] for k in ("value", "unit", "frac", "achieved_gbs", "ms_per_step", "steps",
                                                "alg_bytes_per_launch", "alg_bytes_per_node",
-                                               "traffic", "non_solid_nodes", "porosity", "tile_kernel",
+                                               "traffic", "non_solid_nodes", "porosity", "tile", "tile_kernel",
                                                "gpu_launches", "clocks")}
                 sparse[w]["workload"] = d2
                 del g2
@@ -491,7 +494,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": desc, "layout": layout, "scheme": scheme,
-                   "tile": list(tile) if layout in ("tile", "pointer_tile") else None,
+                   "tile": dev["tile"],
                    "tile_kernel": (("warp work list" if st.tile_work_list else "CTA per tile")
                                    if layout in ("tile", "pointer_tile") else None),
                    "nodes": int(st.n_nodes),

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib
 from .lattice import Q
-from .layouts import LayoutKind, NodeType
+from .layouts import DEFAULT_TILE, LayoutKind, NodeType, default_tile
 
 _SOLID = int(NodeType.SOLID)
 
@@ -274,7 +274,7 @@ class Simulation:
     (reference kernel.py:155-311)."""
 
     def __init__(self, geometry, params, layout=LayoutKind.DENSE, scalar=np.float64,
-                 device=0, tile=(4, 4, 8), slab=None, scheme="ab"):
+                 device=0, tile=None, slab=None, scheme="ab"):
         self.geometry = geometry
         self.params = params
         self.layout = LayoutKind.parse(layout)
@@ -282,11 +282,14 @@ class Simulation:
         if self.dtype not in (np.dtype(np.float32), np.dtype(np.float64)):
             raise ValueError(f"scalar must be float32 or float64, got {scalar}")
         self.device = int(device)
-        self.tile = tuple(int(t) for t in tile)
         # "ab": two buffers swapped every step (the reference's PdfField);
         # "aa": one buffer updated in place (half the memory, same results)
         self.scheme = str(scheme).lower()
         desc = geometry.descriptors
+        if tile is None:
+            # z-slabs cut on tile planes: every rank keeps the fixed default
+            tile = DEFAULT_TILE if slab is not None else default_tile(desc.type_tag, self.layout, self.scheme)
+        self.tile = tuple(int(t) for t in tile)
         self.slab = slab
         nzg, z0, glo, ghi = (None, 0, None, None) if slab is None else \
             (slab.nz_global, slab.z0, slab.ghost_lo, slab.ghost_hi)

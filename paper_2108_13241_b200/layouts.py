@@ -190,6 +190,55 @@ class NodeDescriptorField:
 
 
 # ---------------------------------------------------------------------------
+# default tile shape (the reference takes one fixed tile edge per layout,
+# layouts.py:389-401; here the facade picks between two measured shapes)
+
+DEFAULT_TILE = (4, 4, 8)
+SPARSE_TILE = (4, 4, 4)
+# node fill of the kept 4x4x8 tiles below which 4x4x4 tiles step faster with
+# the AB scheme (profiles/ab_tile_fill_r02al.txt: +4 % at fill 0.49, +2.5 % at
+# 0.59, +0.5 % at 0.67-0.68, -2.4 % at 0.79, -2.5 % at 0.89; level under A-A)
+SPARSE_TILE_FILL = 0.70
+
+
+def kept_tile_fill(type_tag, tile=DEFAULT_TILE):
+    """Non-solid nodes / nodes of the kept tiles (tiles holding at least one
+    non-solid node) for `type_tag` (z, y, x) cut into `tile` = (x, y, z)
+    edges, or None when the extents are not multiples of the edges.  The
+    x-any uses word views (4 bytes = 4 x-neighbours), 0.3 s for 1024^3."""
+    t = np.ascontiguousarray(type_tag, dtype=np.uint8)
+    ex, ey, ez = (int(e) for e in tile)
+    nz, ny, nx = t.shape
+    if ex != 4 or ny % ey or nz % ez or nx % 4:
+        return None
+    x = t.view(np.uint32)                                  # (nz, ny, nx / 4)
+    y = x.reshape(nz, ny // ey, ey, nx // 4)
+    acc = y[:, :, 0].copy()
+    for j in range(1, ey):
+        acc |= y[:, :, j]
+    z = acc.reshape(nz // ez, ez, ny // ey, nx // 4)
+    kept = z[:, 0].copy()
+    for j in range(1, ez):
+        kept |= z[:, j]
+    n_kept = int(np.count_nonzero(kept))
+    if n_kept == 0:
+        return None
+    live = t.size - int(np.count_nonzero(t == NodeType.SOLID))
+    return live / (n_kept * ex * ey * ez)
+
+
+def default_tile(type_tag, layout, scheme="ab"):
+    """Tile shape used when the caller names none: 4x4x8, or 4x4x4 for the
+    compacted tile list under the AB scheme when the kept 4x4x8 tiles are
+    less than SPARSE_TILE_FILL non-solid (low-porosity media, where smaller
+    tiles hug the solid and the step streams faster)."""
+    if LayoutKind.parse(layout) is not LayoutKind.POINTER_TILE or str(scheme).lower() != "ab":
+        return DEFAULT_TILE
+    fill = kept_tile_fill(type_tag, DEFAULT_TILE)
+    return SPARSE_TILE if fill is not None and fill < SPARSE_TILE_FILL else DEFAULT_TILE
+
+
+# ---------------------------------------------------------------------------
 # copy micro-benchmark (reference layouts.py:439-524), on the device
 
 

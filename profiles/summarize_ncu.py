@@ -2,7 +2,7 @@
 profiles/ncu_summary.json (read by bench.py for roofline.traffic) and
 profiles/ncu_<tag>.md.
 
-    python profiles/summarize_ncu.py <tag> [--dtype f32] [--scheme ab] [--tile 4,8,16] [workload ...]
+    python profiles/summarize_ncu.py <tag> [--dtype f32] [--scheme ab] [--tile x,y,z (default: from the capture's bench line)] [workload ...]
 
 Entries are keyed by (workload, dtype, scheme, tile, kernel): bench.py only
 takes `roofline.traffic` from a capture of the same configuration.
@@ -68,9 +68,19 @@ def raw(rep):
 DENSE = ("channel512", "cavity64", "c5", "duct")
 
 
+def logged_tile(tag, w):
+    """The tile the captured bench run used: config.tile of its JSON line
+    (ncu_<tag>_<w>.log, written by profile.sh)."""
+    with open(os.path.join(OUT, f"ncu_{tag}_{w}.log")) as fh:
+        for line in fh:
+            if line.startswith("{"):
+                return json.loads(line)["config"]["tile"]
+    raise SystemExit(f"no bench line in ncu_{tag}_{w}.log: pass --tile")
+
+
 def main():
     argv = sys.argv[1:]
-    opts = {"--dtype": "f32", "--scheme": "ab", "--tile": "4,8,16"}
+    opts = {"--dtype": "f32", "--scheme": "ab", "--tile": "log"}
     rest = []
     while argv:
         a = argv.pop(0)
@@ -93,7 +103,12 @@ def main():
             continue
         k = raw(rep)[0]
         traffic = k["dram_read"] + k["dram_write"]
-        tile = None if w.split("@")[0] in DENSE else [int(v) for v in opts["--tile"].split(",")]
+        if w.split("@")[0] in DENSE:
+            tile = None
+        elif opts["--tile"] == "log":
+            tile = logged_tile(tag, w)
+        else:
+            tile = [int(v) for v in opts["--tile"].split(",")]
         e = {"workload": w, "dtype": opts["--dtype"], "scheme": opts["--scheme"], "tile": tile,
              "tag": tag, "kernel": k["kernel"].split("(")[0],
              "duration_ms": k["duration"] * 1e3, "dram_bytes_per_launch": traffic,

@@ -466,6 +466,8 @@ def test_default_tile_kernel_choice_is_bitwise(phi):
     geom = lb.build_porous_random(64, phi, seed=2, radius_range=(3, 9), dims=(64, 48, 32))
     params = lb.FlowParams.from_viscosity(U=0.05, L=47, nu=0.2)
     sim = lb.Simulation(geom, params, layout="pointer_tile", scalar=np.float32)   # the default tile
+    assert sim.tile == lb.default_tile(geom.descriptors.type_tag, "pointer_tile")
+    assert sim.tile == ((4, 4, 4) if phi <= 0.5 else (4, 4, 8))
     # live-brick fraction of the kept tiles (2x2x2 bricks), as the library computes it
     ex, ey, ez = sim.tile
     ns = geom.descriptors.type_tag != lb.NodeType.SOLID

@@ -216,3 +216,35 @@ def test_periodic_axis_must_divide_tile_without_device():
         lb.Simulation(geom, params, layout="pointer_tile", tile=(8, 4, 4))
     with pytest.raises(ValueError, match="scalar"):
         lb.Simulation(geom, params, layout="dense", scalar=np.float16)
+
+
+def test_kept_tile_fill_matches_brute_force():
+    """The word-view fill count behind the default tile choice equals a
+    plain reshape count of kept tiles, for 4 x {2,4} x {4,8} tiles."""
+    rng = np.random.default_rng(5)
+    for p in (0.02, 0.3, 0.9):
+        t = (rng.random((16, 12, 20)) < p).astype(np.uint8) * rng.integers(1, 5, (16, 12, 20), dtype=np.uint8)
+        live = t != lb.NodeType.SOLID
+        for tile in ((4, 4, 8), (4, 4, 4), (4, 2, 4), (4, 4, 16)):
+            ex, ey, ez = tile
+            nz, ny, nx = t.shape
+            got = lb.kept_tile_fill(t, tile)
+            if nz % ez or ny % ey:
+                assert got is None
+                continue
+            k = live.reshape(nz // ez, ez, ny // ey, ey, nx // ex, ex).any(axis=(1, 3, 5))
+            assert got == pytest.approx(live.sum() / (k.sum() * ex * ey * ez), rel=1e-12)
+    assert lb.kept_tile_fill(np.zeros((8, 4, 4), np.uint8)) is None           # no kept tile
+    assert lb.kept_tile_fill(np.ones((8, 4, 6), np.uint8)) is None            # x not a multiple of 4
+
+
+def test_default_tile_rule():
+    """4x4x4 for the compacted tile list under AB when the kept 4x4x8 tiles are
+    < 70 % non-solid; 4x4x8 otherwise (A-A, other layouts, dense media)."""
+    sparse = lb.build_porous_random(64, 0.1, seed=0, radius_range=(3, 9)).descriptors.type_tag
+    dense = lb.build_porous_random(64, 0.9, seed=0, radius_range=(3, 9)).descriptors.type_tag
+    assert lb.kept_tile_fill(sparse) < 0.70 < lb.kept_tile_fill(dense)
+    assert lb.default_tile(sparse, "pointer_tile") == (4, 4, 4)
+    assert lb.default_tile(sparse, "pointer_tile", scheme="aa") == (4, 4, 8)
+    assert lb.default_tile(sparse, "tile") == (4, 4, 8)
+    assert lb.default_tile(dense, "pointer_tile") == (4, 4, 8)
