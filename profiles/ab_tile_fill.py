@@ -15,6 +15,7 @@ import paper_2108_13241_b200 as lb  # noqa: E402
 SHAPES = [tuple(int(v) for v in t.split(",")) for t in
           os.environ.get("SHAPES", "4,4,8 4,4,4 2,4,4 2,4,8").split()]
 SCHEME = os.environ.get("SCHEME", "ab")
+SCALAR = np.dtype(os.environ.get("SCALAR", "float32"))
 
 
 def fill(live, t):
@@ -30,10 +31,10 @@ for w in sys.argv[1:]:
     fills = {str(t): round(fill(live, t), 4) for t in SHAPES}
     for rep in range(2):
         for t in SHAPES:
-            sim = lb.Simulation(geom, params, layout=layout, scalar=np.float32, tile=t, scheme=SCHEME)
+            sim = lb.Simulation(geom, params, layout=layout, scalar=SCALAR, tile=t, scheme=SCHEME)
             sim.initialize(rho0)
             r = lb.benchmark(sim, 50, 500)
-            print(json.dumps({"workload": w, "tile": t, "rep": rep, "scheme": SCHEME, "mlups": round(r.p_lups / 1e6),
+            print(json.dumps({"workload": w, "tile": t, "rep": rep, "scheme": SCHEME, "scalar": SCALAR.name, "mlups": round(r.p_lups / 1e6),
                               "frac": round(r.u_b_with_flags, 4), "fill": fills[str(t)],
                               "work_list": bool(sim._handle.stats().tile_work_list)}), flush=True)
             sim.close()

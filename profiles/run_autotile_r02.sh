@@ -3,7 +3,7 @@
 # non-solid): GPU suite, smoke, the driver's bench command, the porosity sweep
 # with the default tile, ncu captures keyed by the tile each run used.
 set -u
-TAG=${1:-r02am}
+TAG=${1:-r02an}
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -x -q --durations=8 > gpurun_out/pytest_gpu_${TAG}.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu_${TAG}.log
