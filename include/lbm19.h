@@ -81,7 +81,7 @@ typedef struct lbm_desc {
   int32_t periodic[3];    /* per axis x, y, z */
   int32_t dtype;          /* LBM_F32 / LBM_F64 */
   int32_t layout;         /* LBM_LAYOUT_* */
-  int32_t tile[3];        /* tile edge lengths for tile layouts (powers of two, 32..512 nodes; the Python facade defaults to 4,4,8) */
+  int32_t tile[3];        /* tile edge lengths for tile layouts (powers of two, 32..512 nodes; the Python facade picks 4,4,8, or 4,4,4 for sparse tile lists: layouts.default_tile) */
   int32_t device;         /* CUDA device ordinal */
   double omega;           /* BGK collision frequency, cast to dtype */
   int32_t scheme;         /* LBM_SCHEME_AB (two buffers) / LBM_SCHEME_AA (one, in place) */
