@@ -208,3 +208,29 @@ def test_slabs_two_processes_ipc_bitwise(tmp_path, layout):
     single.step(25)
     got = np.concatenate([np.load(tmp_path / f"ipc{r}.npy") for r in range(2)], axis=1)
     assert np.array_equal(got, single.canonical_state())
+
+
+def test_default_tile_on_slabs_is_fixed():
+    """tile=None: a single domain of a low-fill medium takes 4x4x4 tiles, z-slabs
+    of the same medium keep 4x4x8 (every rank cuts on the same tile planes), and
+    the AB work-list slabs with that default reproduce the single domain bitwise."""
+    geom = lb.build_porous_random(32, 0.15, seed=1, radius_range=(2, 6), dims=(32, 16, 32))
+    params = lb.FlowParams.from_viscosity(U=0.05, L=15, nu=0.2)
+    single = lb.Simulation(geom, params, layout="pointer_tile", scalar=np.float32)
+    assert single.tile == (4, 4, 4)
+    single.initialize(1.004)
+    sims = []
+    for z0, z1 in split_z_balanced(geom.descriptors.type_tag, 2, align=lb.layouts.DEFAULT_TILE[2]):
+        g, spec = slab_geometry(geom, z0, z1)
+        sims.append(lb.Simulation(g, params, layout="pointer_tile", scalar=np.float32, slab=spec))
+        assert sims[-1].tile == (4, 4, 8)
+    connect_local(sims, geom.periodic[2])
+    for s in sims:
+        s.initialize(1.004)
+    single.step(7)
+    for s in sims:
+        s.step(7, block=False)    # slabs step together: a blocking step would wait on its neighbour
+    for s in sims:
+        s.synchronize()
+    got = np.concatenate([s.canonical_state() for s in sims], axis=1)
+    assert np.array_equal(got, single.canonical_state())
