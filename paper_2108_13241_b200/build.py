@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "liblbm19.so")
-SOURCES = [os.path.join(CSRC, "lbm19.cu")]
+SOURCES = [os.path.join(CSRC, "lbm19.cu"), os.path.join(CSRC, "host_copy.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cuh")] + \
     [os.path.join(ROOT, "include", "lbm19.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

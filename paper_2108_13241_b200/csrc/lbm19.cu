@@ -730,6 +730,8 @@ static int ensure_pinned(lbm_handle* h, size_t bytes) {
 }
 // host copy split over threads (also spreads the page faults of fresh
 // destination arrays)
+__attribute__((visibility("hidden"))) void lbm_bulk_copy(char* d, const char* s, size_t n);  // host_copy.cpp
+
 static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
   size_t total = 0;
   for (size_t v : n) total += v;
@@ -741,7 +743,7 @@ static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, 
   auto work = [&](int t) {
     for (size_t k = 0; k < n.size(); ++k) {
       const size_t per = (n[k] + nt - 1) / nt, a = per * t, b = a + per < n[k] ? a + per : n[k];
-      if (a < b) memcpy(dst_src[k].first + a, dst_src[k].second + a, b - a);
+      if (a < b) lbm_bulk_copy(dst_src[k].first + a, dst_src[k].second + a, b - a);
     }
   };
   if (nt == 1) {
