@@ -34,6 +34,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cstring>
 #include <unistd.h>
 #include <sys/mman.h>
@@ -732,6 +734,55 @@ static int ensure_pinned(lbm_handle* h, size_t bytes) {
 // destination arrays)
 __attribute__((visibility("hidden"))) void lbm_bulk_copy(char* d, const char* s, size_t n);  // host_copy.cpp
 
+// Persistent copy workers, parked on a condition variable between calls: a
+// readback copies 64 staging chunks, and spawning + joining 15 threads per
+// chunk was a visible part of its host time.  Created on first use and never
+// torn down (detached); one call at a time.
+class CopyPool {
+ public:
+  explicit CopyPool(int workers) : nw_(workers) {
+    for (int t = 1; t <= nw_; ++t) std::thread([this, t] { loop(t); }).detach();
+  }
+  int size() const { return nw_ + 1; }
+  // runs f(0) .. f(nw) -- f(0) on the calling thread -- and returns when all finished
+  void run(const std::function<void(int)>& f) {
+    std::lock_guard<std::mutex> one(run_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      pending_ = nw_;
+      ++gen_;
+    }
+    go_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void loop(int t) {
+    long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        go_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        f = job_;
+      }
+      (*f)(t);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  const int nw_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable go_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  long gen_ = 0;
+  int pending_ = 0;
+};
+
 static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, const std::vector<size_t>& n) {
   size_t total = 0;
   for (size_t v : n) total += v;
@@ -739,8 +790,12 @@ static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, 
     const unsigned c = std::thread::hardware_concurrency();
     return c == 0 ? 8 : (c > 16 ? 16 : (int)c);
   }();
+  static const bool pooled = [] {
+    const char* v = getenv("LBM_COPY_POOL");
+    return !(v && v[0] == '0');
+  }();
   const int nt = total > (8u << 20) ? hw : 1;
-  auto work = [&](int t) {
+  const std::function<void(int)> work = [&](int t) {
     for (size_t k = 0; k < n.size(); ++k) {
       const size_t per = (n[k] + nt - 1) / nt, a = per * t, b = a + per < n[k] ? a + per : n[k];
       if (a < b) lbm_bulk_copy(dst_src[k].first + a, dst_src[k].second + a, b - a);
@@ -748,6 +803,24 @@ static void par_copy(const std::vector<std::pair<char*, const char*>>& dst_src, 
   };
   if (nt == 1) {
     work(0);
+    return;
+  }
+  if (pooled) {
+    // leaked on purpose (detached workers outlive main); a forked child has no
+    // workers, so it starts its own pool
+    static std::mutex mu;
+    static CopyPool* pool = nullptr;
+    static pid_t owner = 0;
+    CopyPool* p;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!pool || owner != getpid()) {
+        pool = new CopyPool(hw - 1);
+        owner = getpid();
+      }
+      p = pool;
+    }
+    p->run(work);
     return;
   }
   std::vector<std::thread> th;
